@@ -1,0 +1,408 @@
+// analysis.cu -- setup and analysis kernels of libmpgabor (sm_100a):
+//   windows (O2 reading Z1/Z2), twiddle/root tables, signal padding + energy,
+//   N1 DGT analysis, N2 Gram cross-kernel precompute + threshold +
+//   compaction (Eqs. (14)-(17); Eq. (7)), N4 tile-max init.
+#include <algorithm>
+#include "launch.h"
+#include "fft.cuh"
+#include "argmax.cuh"
+
+// ---------------------------------------------------------------------------
+// windows: g(j), j = -floor(gl/2) .. ceil(gl/2)-1, unit norm
+// ---------------------------------------------------------------------------
+__global__ void window_kernel(int win, int gl, int a, int M, double* __restrict__ g) {
+  __shared__ double part[1024];
+  const int j0 = -(gl / 2);
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < gl; i += blockDim.x) {
+    const double j = (double)(j0 + i);
+    double v;
+    if (win == 1) v = 0.5 + 0.5 * cospi(2.0 * j / gl);
+    else if (win == 2) v = 0.42 + 0.5 * cospi(2.0 * j / gl) + 0.08 * cospi(4.0 * j / gl);
+    else v = exp(-M_PI * j * j / ((double)a * (double)M));
+    g[i] = v;
+    acc += v * v;
+  }
+  part[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) part[threadIdx.x] += part[threadIdx.x + s];
+    __syncthreads();
+  }
+  const double inv = 1.0 / sqrt(part[0]);
+  for (int i = threadIdx.x; i < gl; i += blockDim.x) g[i] *= inv;
+}
+
+// tw[k] = e^{-2 pi i k / res}, k < res/2 ;  roots[r] = e^{+2 pi i r / R}, r < R
+__global__ void tables_kernel(double2* __restrict__ tw, int twres, double2* __restrict__ roots, int R) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < twres / 2) {
+    double s, c;
+    sincospi(-2.0 * (double)i / (double)twres, &s, &c);
+    tw[i] = make_double2(c, s);
+  }
+  if (i < R) {
+    double s, c;
+    sincospi(2.0 * (double)i / (double)R, &s, &c);
+    roots[i] = make_double2(c, s);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// padding, finiteness and E0 = ||x||^2 (Alg. 1 init); deterministic
+// two-stage reduction (fixed block partition, fixed tree order)
+// ---------------------------------------------------------------------------
+__global__ void pad_energy_kernel(const double* __restrict__ x, int64_t Ls, double* __restrict__ xp, int64_t L,
+                                  double* __restrict__ partial, int* __restrict__ nonfinite) {
+  __shared__ double sh[256];
+  double acc = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < L; i += (int64_t)gridDim.x * blockDim.x) {
+    double v = i < Ls ? x[i] : 0.0;
+    if (!isfinite(v)) { *nonfinite = 1; v = 0.0; }
+    xp[i] = v;
+    acc += v * v;
+  }
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
+}
+
+__global__ void sum_partials_kernel(const double* __restrict__ partial, int n, double* __restrict__ out) {
+  __shared__ double sh[256];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) acc += partial[i];
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sh[0];
+}
+
+// ---------------------------------------------------------------------------
+// N1 DGT: c(m,n) = sum_j x(na+j) g(j) e^{-2 pi i m j/M}, m = 0..M/2 (Eq. (3)),
+// frames folded mod M then one real FFT of length M per frame in shared memory.
+// F frames per CTA.  Output row stride `stride` (>= M/2+1, zero padded).
+// ---------------------------------------------------------------------------
+template <typename R>
+__global__ void dgt_kernel(const double* __restrict__ x, int64_t L, int a, int M, int gl, int N,
+                           const double* __restrict__ g, const double2* __restrict__ tw, int twres,
+                           typename cplx<R>::t* __restrict__ out, int stride, int F) {
+  using C2 = typename cplx<R>::t;
+  extern __shared__ double2 z[];
+  const int n = M / 2;
+  const int lgn = 31 - __clz(n);
+  const int j0 = -(gl / 2);
+  const int frame0 = blockIdx.x * F;
+  for (int idx = threadIdx.x; idx < F * M; idx += blockDim.x) {
+    const int f = idx / M, s = idx - f * M;
+    const int frame = frame0 + f;
+    double v = 0.0;
+    if (frame < N) {
+      const int64_t base = (int64_t)frame * a;
+      for (int j = j0 + fmod32(s - j0, M); j < j0 + gl; j += M) v += x[fmod64(base + j, L)] * g[j - j0];
+    }
+    double* zz = reinterpret_cast<double*>(&z[f * n + bitrev(s >> 1, lgn)]);
+    zz[s & 1] = v;
+  }
+  __syncthreads();
+  smem_fft(z, lgn, F, tw, twres, -1);
+  for (int idx = threadIdx.x; idx < F * stride; idx += blockDim.x) {
+    const int f = idx / stride, m = idx - f * stride;
+    const int frame = frame0 + f;
+    if (frame >= N) continue;
+    C2 o;
+    if (m <= n) {
+      const double2 X = rfft_bin(z + f * n, lgn, m, tw, twres);
+      o.x = (R)X.x;
+      o.y = (R)X.y;
+    } else {
+      o.x = 0;
+      o.y = 0;
+    }
+    out[(int64_t)frame * stride + m] = o;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// N2 kernel rows: for lag nu = nu_first + blockIdx.x
+//   b[s mod M_c] += g_u(s + nu a_c) g_v(s),  H[i][m] = sum_s b e^{-2 pi i m s/M_c}, m = 0..M_c/2
+// i.e. h_{u,v}(m, nu) for m >= 0 (h(-m,nu) = conj h(m,nu), real windows).
+// ---------------------------------------------------------------------------
+__global__ void kern_rows_kernel(int a_c, int M_c, int nu_first, const double* __restrict__ gu, int glu,
+                                 const double* __restrict__ gv, int glv, const double2* __restrict__ tw,
+                                 int twres, double2* __restrict__ H) {
+  extern __shared__ double2 z[];
+  const int n = M_c / 2;
+  const int lgn = 31 - __clz(n);
+  const int nu = nu_first + blockIdx.x;
+  const int ju0 = -(glu / 2), ju1 = ju0 + glu - 1;
+  const int jv0 = -(glv / 2), jv1 = jv0 + glv - 1;
+  const int slo = max(jv0, ju0 - nu * a_c), shi = min(jv1, ju1 - nu * a_c);
+  for (int r = threadIdx.x; r < M_c; r += blockDim.x) {
+    double v = 0.0;
+    if (slo <= shi)
+      for (int s = slo + fmod32(r - slo, M_c); s <= shi; s += M_c) v += gu[s + nu * a_c - ju0] * gv[s - jv0];
+    double* zz = reinterpret_cast<double*>(&z[bitrev(r >> 1, lgn)]);
+    zz[r & 1] = v;
+  }
+  __syncthreads();
+  smem_fft(z, lgn, 1, tw, twres, -1);
+  double2* row = H + (int64_t)blockIdx.x * (n + 1);
+  for (int m = threadIdx.x; m <= n; m += blockDim.x) row[m] = rfft_bin(z, lgn, m, tw, twres);
+}
+
+__device__ __forceinline__ double cabs2(double2 v) { return sqrt(v.x * v.x + v.y * v.y); }
+
+// max |h| over the pair (order independent: max of non-negative doubles via their bit patterns)
+__global__ void kern_max_kernel(const double2* __restrict__ H, int64_t count, unsigned long long* __restrict__ mx) {
+  double m = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+    m = fmax(m, cabs2(H[i]));
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(mx, (unsigned long long)__double_as_longlong(m));
+}
+
+// bounding box of entries with |h| > thr * max (strict, relative; Z5-Z7), signed mu in (-M_c/2, M_c/2]
+// box[0..3] = mu_lo, mu_hi, nu_lo, nu_hi (init to +inf,-inf,+inf,-inf); box[4] += kept count
+__global__ void kern_box_kernel(const double2* __restrict__ H, int nlag, int M_c, int nu_first, double thr,
+                                const unsigned long long* __restrict__ mxp, int* __restrict__ box) {
+  const int n = M_c / 2;
+  const double lim = thr * __longlong_as_double((long long)*mxp);
+  const int64_t count = (int64_t)nlag * (n + 1);
+  int mlo = INT_MAX, mhi = INT_MIN, nlo = INT_MAX, nhi = INT_MIN, kept = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    if (cabs2(H[i]) > lim) {
+      const int row = (int)(i / (n + 1)), m = (int)(i - (int64_t)row * (n + 1));
+      const int nu = nu_first + row;
+      const bool mirror = (m > 0 && m < n);
+      mhi = max(mhi, m);
+      mlo = min(mlo, mirror ? -m : m);
+      nlo = min(nlo, nu);
+      nhi = max(nhi, nu);
+      kept += mirror ? 2 : 1;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mlo = min(mlo, __shfl_xor_sync(0xffffffffu, mlo, o));
+    mhi = max(mhi, __shfl_xor_sync(0xffffffffu, mhi, o));
+    nlo = min(nlo, __shfl_xor_sync(0xffffffffu, nlo, o));
+    nhi = max(nhi, __shfl_xor_sync(0xffffffffu, nhi, o));
+    kept += __shfl_xor_sync(0xffffffffu, kept, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&box[0], mlo);
+    atomicMax(&box[1], mhi);
+    atomicMin(&box[2], nlo);
+    atomicMax(&box[3], nhi);
+    atomicAdd(&box[4], kept);
+  }
+}
+
+// Compact the box into the per-alignment-class layout of PairGeo:
+// class (on, om) = (i_nu mod s_n, i_mu mod s_m) holds rows i_nu = on + r s_n and
+// columns i_mu = om + c s_m as a contiguous [nr(on)][nc(om)] block at
+// koff + cnt_lt(on) * nmu + nr(on) * cnt_lt(om).  Sub-threshold entries are 0.
+// Also writes the fp64 box copy (row-major [nu][mu]) used by parity tests and
+// the fp64 conjugate-pair row (nu = 0) when u == v.
+template <typename R>
+__global__ void kern_compact_kernel(const double2* __restrict__ H, int M_c, int nu_first, double thr,
+                                    const unsigned long long* __restrict__ mxp, PairGeo pg,
+                                    typename cplx<R>::t* __restrict__ kern, double2* __restrict__ boxcopy,
+                                    RhoEnt* __restrict__ rho_row) {
+  using C2 = typename cplx<R>::t;
+  const int n = M_c / 2;
+  const double lim = thr * __longlong_as_double((long long)*mxp);
+  const int64_t count = (int64_t)pg.nmu * pg.nnu;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    const int inu = (int)(i / pg.nmu), imu = (int)(i - (int64_t)inu * pg.nmu);
+    const int mu = pg.mu_lo + imu, nu = pg.nu_lo + inu;
+    const int m = mu < 0 ? -mu : mu;
+    double2 v = H[(int64_t)(nu - nu_first) * (n + 1) + m];
+    if (mu < 0) v.y = -v.y;
+    if (!(cabs2(v) > lim)) v = make_double2(0.0, 0.0);
+    const int on = inu % pg.s_n, r = inu / pg.s_n;
+    const int om = imu % pg.s_m, c = imu / pg.s_m;
+    const int nr = cnt_eq(on, pg.nnu, pg.s_n), nc = cnt_eq(om, pg.nmu, pg.s_m);
+    const int64_t dst = pg.koff + (int64_t)cnt_lt(on, pg.nnu, pg.s_n) * pg.nmu +
+                        (int64_t)nr * cnt_lt(om, pg.nmu, pg.s_m) + (int64_t)r * nc + c;
+    C2 o;
+    o.x = (R)v.x;
+    o.y = (R)v.y;
+    kern[dst] = o;
+    if (boxcopy) boxcopy[i] = v;
+    if (rho_row && nu == 0) {
+      RhoEnt e;
+      e.re = v.x;
+      e.im = v.y;
+      e.inv = 1.0 / (1.0 - (v.x * v.x + v.y * v.y));
+      e.pad_ = 0.0;
+      rho_row[imu] = e;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// N4 init: one warp per tile computes the tile record (best |c|^2, lowest index)
+// and stores it at rec[(g % C) * Lc + g / C] (CTA-major slices of the loop kernel).
+// ---------------------------------------------------------------------------
+template <typename R>
+__device__ __forceinline__ R score_of(R re, R im);
+template <>
+__device__ __forceinline__ double score_of<double>(double re, double im) {
+  return __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im));
+}
+template <>
+__device__ __forceinline__ float score_of<float>(float re, float im) {
+  return __fadd_rn(__fmul_rn(re, re), __fmul_rn(im, im));
+}
+
+template <typename R, int TW>
+__global__ void tile_init_kernel(const typename cplx<R>::t* __restrict__ grid, const DictGeo* __restrict__ dg,
+                                 const OwnGeo* __restrict__ own, int W, int64_t total, int C, int64_t Lc,
+                                 Rec<R>* __restrict__ rec) {
+  // tile g of dictionary v, frame n goes to its owner CTA c = (frame_off_v + n) mod C,
+  // local index loc_base(c,v) + ((n - n_first(c,v)) / C) * T_v + t (frame-major)
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g < total; g += nwarps) {
+    Rec<R> best = empty_rec(R(0));
+    int64_t dst;
+    {
+      int v = 0;
+      while (v + 1 < W && dg[v + 1].tile_off <= g) ++v;
+      const DictGeo d = dg[v];
+      const int64_t loc = g - d.tile_off;
+      const int64_t n = loc / d.T;
+      const int t = (int)(loc - n * d.T);
+      const int c = (int)((d.frame_off + n) % C);
+      const OwnGeo o = own[c * W + v];
+      dst = (int64_t)c * Lc + o.loc_base + ((n - o.n_first) / C) * d.T + t;
+      const typename cplx<R>::t* row = grid + d.grid_off + n * d.stride;
+#pragma unroll
+      for (int ch = 0; ch < TW / 32; ++ch) {
+        const int b = t * TW + ch * 32 + lane;
+        if (b < d.MR) {
+          const typename cplx<R>::t c = row[b];
+          const R s = score_of<R>(c.x, c.y);
+          const uint32_t p = (uint32_t)(d.off + n * d.MR + b);
+          if (better(s, p, best.s, best.p)) {
+            best.s = s;
+            best.p = p;
+            best.re = c.x;
+            best.im = c.y;
+          }
+        }
+      }
+    }
+    best = warp_best(best);
+    if (lane == 0) rec[dst] = best;
+  }
+}
+
+// empty records in every slot (run before tile_init_kernel: slices are padded to Lc)
+template <typename R>
+__global__ void rec_clear_kernel(Rec<R>* __restrict__ rec, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    rec[i] = empty_rec(R(0));
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+cudaError_t launch_window(int win, int gl, int a, int M, double* g, cudaStream_t st) {
+  window_kernel<<<1, 1024, 0, st>>>(win, gl, a, M, g);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tables(double2* tw, int twres, double2* roots, int R, cudaStream_t st) {
+  const int n = max(twres / 2, R);
+  tables_kernel<<<(n + 255) / 256, 256, 0, st>>>(tw, twres, roots, R);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pad_energy(const double* x, int64_t Ls, double* xp, int64_t L, double* partial,
+                              int* nonfinite, double* E0, cudaStream_t st) {
+  pad_energy_kernel<<<256, 256, 0, st>>>(x, Ls, xp, L, partial, nonfinite);
+  sum_partials_kernel<<<1, 256, 0, st>>>(partial, 256, E0);
+  return cudaGetLastError();
+}
+
+static int dgt_frames_per_cta(int M) { return max(1, 2048 / (M / 2)); }
+
+template <typename R>
+cudaError_t launch_dgt(const double* xp, int64_t L, const DictGeo& d, const double* g, const double2* tw,
+                       int twres, typename cplx<R>::t* out, cudaStream_t st) {
+  const int F = dgt_frames_per_cta(d.M);
+  const size_t smem = (size_t)F * (d.M / 2) * sizeof(double2);
+  static bool attr = false;
+  if (!attr) {
+    CUDA_OK(cudaFuncSetAttribute(dgt_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr = true;
+  }
+  dgt_kernel<R><<<(d.N + F - 1) / F, 256, smem, st>>>(xp, L, d.a, d.M, d.gl, d.N, g, tw, twres, out, d.stride, F);
+  return cudaGetLastError();
+}
+template cudaError_t launch_dgt<double>(const double*, int64_t, const DictGeo&, const double*, const double2*, int,
+                                        double2*, cudaStream_t);
+template cudaError_t launch_dgt<float>(const double*, int64_t, const DictGeo&, const double*, const double2*, int,
+                                       float2*, cudaStream_t);
+
+cudaError_t launch_kern_rows(int a_c, int M_c, int nu_first, int nlag, const double* gu, int glu, const double* gv,
+                             int glv, const double2* tw, int twres, double2* H, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    CUDA_OK(cudaFuncSetAttribute(kern_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr = true;
+  }
+  const size_t smem = (size_t)(M_c / 2) * sizeof(double2);
+  kern_rows_kernel<<<nlag, 512, smem, st>>>(a_c, M_c, nu_first, gu, glu, gv, glv, tw, twres, H);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_kern_max_box(const double2* H, int nlag, int M_c, int nu_first, double thr,
+                                unsigned long long* mx, int* box, cudaStream_t st) {
+  const int64_t count = (int64_t)nlag * (M_c / 2 + 1);
+  const int blocks = (int)std::min<int64_t>(1184, (count + 255) / 256);
+  kern_max_kernel<<<blocks, 256, 0, st>>>(H, count, mx);
+  kern_box_kernel<<<blocks, 256, 0, st>>>(H, nlag, M_c, nu_first, thr, mx, box);
+  return cudaGetLastError();
+}
+
+template <typename R>
+cudaError_t launch_kern_compact(const double2* H, int M_c, int nu_first, double thr, const unsigned long long* mx,
+                                const PairGeo& pg, typename cplx<R>::t* kern, double2* boxcopy, RhoEnt* rho_row,
+                                cudaStream_t st) {
+  const int64_t count = (int64_t)pg.nmu * pg.nnu;
+  const int blocks = (int)std::min<int64_t>(1184, (count + 255) / 256);
+  kern_compact_kernel<R><<<blocks, 256, 0, st>>>(H, M_c, nu_first, thr, mx, pg, kern, boxcopy, rho_row);
+  return cudaGetLastError();
+}
+template cudaError_t launch_kern_compact<double>(const double2*, int, int, double, const unsigned long long*,
+                                                 const PairGeo&, double2*, double2*, RhoEnt*, cudaStream_t);
+template cudaError_t launch_kern_compact<float>(const double2*, int, int, double, const unsigned long long*,
+                                                const PairGeo&, float2*, double2*, RhoEnt*, cudaStream_t);
+
+template <typename R>
+cudaError_t launch_tile_init(const typename cplx<R>::t* grid, const DictGeo* dg, const OwnGeo* own, int W,
+                             int64_t total, int C, int64_t Lc, int TW, Rec<R>* rec, cudaStream_t st) {
+  const int64_t slots = (int64_t)C * Lc;
+  rec_clear_kernel<R><<<(int)std::min<int64_t>(1184, (slots + 255) / 256), 256, 0, st>>>(rec, slots);
+  const int blocks = (int)std::min<int64_t>(148 * 8, (total + 7) / 8);
+  switch (TW) {
+    case 32: tile_init_kernel<R, 32><<<blocks, 256, 0, st>>>(grid, dg, own, W, total, C, Lc, rec); break;
+    case 64: tile_init_kernel<R, 64><<<blocks, 256, 0, st>>>(grid, dg, own, W, total, C, Lc, rec); break;
+    case 128: tile_init_kernel<R, 128><<<blocks, 256, 0, st>>>(grid, dg, own, W, total, C, Lc, rec); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+template cudaError_t launch_tile_init<double>(const double2*, const DictGeo*, const OwnGeo*, int, int64_t, int,
+                                              int64_t, int, Rec<double>*, cudaStream_t);
+template cudaError_t launch_tile_init<float>(const float2*, const DictGeo*, const OwnGeo*, int, int64_t, int,
+                                             int64_t, int, Rec<float>*, cudaStream_t);

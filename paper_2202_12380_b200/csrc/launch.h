@@ -1,0 +1,81 @@
+// launch.h -- internal launcher declarations of libmpgabor (host side of the CUDA path).
+#pragma once
+#include "common.cuh"
+
+cudaError_t launch_window(int win, int gl, int a, int M, double* g, cudaStream_t st);
+cudaError_t launch_tables(double2* tw, int twres, double2* roots, int R, cudaStream_t st);
+cudaError_t launch_pad_energy(const double* x, int64_t Ls, double* xp, int64_t L, double* partial, int* nonfinite,
+                              double* E0, cudaStream_t st);
+template <typename R>
+cudaError_t launch_dgt(const double* xp, int64_t L, const DictGeo& d, const double* g, const double2* tw, int twres,
+                       typename cplx<R>::t* out, cudaStream_t st);
+cudaError_t launch_kern_rows(int a_c, int M_c, int nu_first, int nlag, const double* gu, int glu, const double* gv,
+                             int glv, const double2* tw, int twres, double2* H, cudaStream_t st);
+cudaError_t launch_kern_max_box(const double2* H, int nlag, int M_c, int nu_first, double thr, unsigned long long* mx,
+                                int* box, cudaStream_t st);
+template <typename R>
+cudaError_t launch_kern_compact(const double2* H, int M_c, int nu_first, double thr, const unsigned long long* mx,
+                                const PairGeo& pg, typename cplx<R>::t* kern, double2* boxcopy, RhoEnt* rho_row,
+                                cudaStream_t st);
+template <typename R>
+cudaError_t launch_tile_init(const typename cplx<R>::t* grid, const DictGeo* dg, const OwnGeo* own, int W,
+                             int64_t total, int C, int64_t Lc, int TW, Rec<R>* rec, cudaStream_t st);
+
+// persistent MP loop (mploop.cu)
+struct AtomOut {  // identical layout to mpg_atom
+  int32_t w, m, n, flags;
+  double re, im;
+};
+struct LoopResult {
+  long long n_done;
+  int stop;
+  int pad;
+  double E_final;
+};
+
+constexpr int MAX_LEVELS = 6;
+constexpr int MAX_CLUSTER = 16;
+constexpr int TOP_SCAN = 256;   // the top node level (<= TOP_SCAN nodes) is scanned by one warp
+
+struct LoopParams {
+  int W, C, TW;
+  int Rmax;
+  int srec;                      // 1: this CTA's tile records live in shared memory
+  int nlev;                      // node levels above the tiles (level l groups 32 of level l-1)
+  int lev_n[MAX_LEVELS];         // node count per level; lev_n[nlev-1] <= TOP_SCAN
+  int lev_off[MAX_LEVELS];       // node offset of each level in the shared level array
+  int rho_total;                 // total entries of the conjugate-pair rows
+  long long Lc;                  // tile records per CTA slice
+  const DictGeo* dicts;          // [W]
+  const OwnGeo* own;             // [C*W] frame ownership of each CTA
+  const PairGeo* pairs;          // [W*W], index u*W + v
+  const double2* roots;          // [Rmax]  e^{2 pi i r/Rmax}
+  const RhoEnt* rho;             // concatenated nu=0 rows of h_uu (fp64) with 1/(1-|rho|^2)
+  const int* rho_lo;             // [W] signed mu of rho[rho_off[u]]
+  const int* rho_n;              // [W]
+  const int* rho_off;            // [W]
+  void* grid;                    // residual grids (cplx<R>)
+  const void* kern;              // kernels (cplx<R>), per-class layout
+  void* rec;                     // Rec<R>[C * Lc] (initial records; the live ones when !srec)
+  long long maxit;
+  double Etol, E0;
+  AtomOut* atoms;
+  double* energy;
+  double2* sol;                  // may be null
+  LoopResult* result;
+  long long* prof;               // optional [8] clock64 phase sums (rank 0, thread 0), [7] = iterations
+  int floor_mode;                // 1: skip the update (latency-floor measurement; results invalid)
+  size_t smem_bytes;
+};
+
+size_t loop_smem_bytes(const LoopParams& P, bool f64);
+cudaError_t launch_mp_loop(const LoopParams& P, bool f64, int threads, cudaStream_t st);
+int loop_max_cluster(bool f64, bool srec, int TW, int threads, size_t smem);
+
+// synthesis (synth.cu)
+cudaError_t launch_synth_scatter(const AtomOut* atoms, int64_t n_atoms, const DictGeo* dg_dev, int W, double2* sol,
+                                 cudaStream_t st);
+cudaError_t launch_synth_frames(const double2* sol, const DictGeo& d, const double2* tw, int twres, double* frames,
+                                cudaStream_t st);
+cudaError_t launch_synth_ola(const double* frames, const DictGeo& d, const double* g, int64_t L, double* y,
+                             int accumulate, cudaStream_t st);

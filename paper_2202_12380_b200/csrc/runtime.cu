@@ -1,0 +1,767 @@
+// runtime.cu -- host runtime and C ABI of libmpgabor (include/mpgabor.h).
+//
+// Owns the handle: dictionary validation, window/twiddle/root tables,
+// kernel precompute orchestration (N2), per-length layout (padding Z3, grids,
+// tiles, tile-record slices), device buffers, launches of N1/N4/N5/N6 and the
+// error strings.  Every arithmetic step of the method runs in the CUDA kernels;
+// this file only computes sizes, offsets and launch geometry.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/mpgabor.h"
+#include "launch.h"
+
+namespace {
+
+thread_local std::string g_create_error = "no error";
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t n) {
+    if (n <= bytes && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&p, n ? n : 16);
+    if (e == cudaSuccess) bytes = n;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <typename T>
+  T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+bool is_pow2(int x) { return x > 0 && (x & (x - 1)) == 0; }
+
+}  // namespace
+
+struct mpgabor {
+  std::vector<mpg_dict> dicts;
+  int W = 0;
+  int precision = MPG_F64;
+  std::string err = "no error";
+  int device = -1;
+
+  // tables
+  int twres = 0, Rmax = 0, a_min = 0, M_max = 0;
+  DevBuf tw, roots, win;
+  std::vector<int64_t> win_off;
+
+  // kernels
+  bool have_kernels = false;
+  double thr = 0.0;
+  std::vector<PairGeo> pairs;
+  std::vector<int> nu_first, nlag;
+  std::vector<double> pair_mx;
+  std::vector<int64_t> pair_kept, box_off;
+  int64_t kern_elems = 0, box_total = 0, kept_total = 0;
+  DevBuf kern, boxcopy, d_pairs, rho, rho_meta, Hscratch, mxbox;
+  std::vector<int> rho_lo, rho_n, rho_off;
+  int rho_total = 0;
+
+  // launch tuning
+  int cluster_req = 0, threads = 512, TW_req = 0, srec_req = 0;  // 0 = automatic
+  int TW = 64, srec = 0;
+
+  // per-length layout
+  int64_t L = -1, Ls_cached = -1;
+  int lay_TW = 0, lay_C = 0;
+  std::vector<DictGeo> geo;
+  std::vector<OwnGeo> own;
+  DevBuf d_own;
+  int64_t grid_elems = 0, total_tiles = 0, Lc = 0, P_R = 0;
+  LoopParams lp{};
+  DevBuf d_geo, grid, rec, xp, partial, flag, E0, result;
+
+  // synth / host-api scratch
+  DevBuf sol, frames, hx, hatoms, henergy, hy;
+
+  int prof_mode = 0;
+  long long prof_host[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  DevBuf prof;
+  cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  float t_dgt = 0, t_init = 0, t_loop = 0;
+
+  int fail(int code, const std::string& msg) {
+    err = msg;
+    return code;
+  }
+  int cuda_fail(cudaError_t e, const char* where) {
+    err = std::string("CUDA error in ") + where + ": " + cudaGetErrorString(e);
+    cudaGetLastError();
+    return e == cudaErrorMemoryAllocation ? MPG_ENOMEM : MPG_ECUDA;
+  }
+  bool f64() const { return precision == MPG_F64; }
+  size_t celem() const { return f64() ? sizeof(double2) : sizeof(float2); }
+};
+
+#define TRY_CUDA(h, expr)                                \
+  do {                                                   \
+    cudaError_t e__ = (expr);                            \
+    if (e__ != cudaSuccess) return (h)->cuda_fail(e__, #expr); \
+  } while (0)
+
+static int enter_device(mpgabor* h) {
+  if (h->device < 0) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+      cudaGetLastError();
+      return h->fail(MPG_ECUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+    }
+    TRY_CUDA(h, cudaGetDevice(&h->device));
+    cudaDeviceProp prop;
+    TRY_CUDA(h, cudaGetDeviceProperties(&prop, h->device));
+    if (prop.major < 10) {
+      h->device = -1;
+      return h->fail(MPG_ECUDA, "libmpgabor is built for sm_100a (B200); device is sm_" +
+                                    std::to_string(prop.major) + std::to_string(prop.minor));
+    }
+    for (auto& e2 : h->ev) TRY_CUDA(h, cudaEventCreate(&e2));
+  } else {
+    TRY_CUDA(h, cudaSetDevice(h->device));
+  }
+  return MPG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// create / destroy / errors
+// ---------------------------------------------------------------------------
+extern "C" int mpgabor_create(const mpg_dict* dicts, int32_t W, int32_t precision, mpgabor** out) {
+  if (out) *out = nullptr;
+  if (!dicts || !out) return g_create_error = "null pointer", MPG_EINVAL;
+  if (W < 1 || W > MPG_MAX_DICTS) return g_create_error = "W must be in [1, 16]", MPG_EINVAL;
+  if (precision != MPG_F64 && precision != MPG_F32) return g_create_error = "precision must be MPG_F64 or MPG_F32", MPG_EINVAL;
+  for (int w = 0; w < W; ++w) {
+    const mpg_dict& d = dicts[w];
+    if (d.win < MPG_WIN_HANN || d.win > MPG_WIN_GAUSS)
+      return g_create_error = "dictionary " + std::to_string(w) + ": unknown window", MPG_EINVAL;
+    if (d.gl < 1 || d.a < 1 || d.M < 1 || d.gl > (1 << 20))
+      return g_create_error = "dictionary " + std::to_string(w) + ": gl, a, M must be >= 1", MPG_EINVAL;
+    if (!is_pow2(d.M) || d.M < 2 || d.M > 16384)
+      return g_create_error = "dictionary " + std::to_string(w) + ": M must be a power of two in [2, 16384]", MPG_EINVAL;
+    if (d.M % d.a)
+      return g_create_error = "dictionary " + std::to_string(w) + ": M/a must be an integer (P:300-301)", MPG_EINCOMPAT;
+  }
+  for (int u = 0; u < W; ++u)
+    for (int v = 0; v < W; ++v) {
+      const mpg_dict &du = dicts[u], &dv = dicts[v];
+      if (std::max(du.a, dv.a) % std::min(du.a, dv.a) || std::max(du.M, dv.M) % std::min(du.M, dv.M))
+        return g_create_error = "dictionaries " + std::to_string(u) + "," + std::to_string(v) +
+                                " are not compatible (P:296-303)",
+               MPG_EINCOMPAT;
+    }
+  mpgabor* h = new mpgabor();
+  h->dicts.assign(dicts, dicts + W);
+  h->W = W;
+  h->precision = precision;
+  h->a_min = dicts[0].a;
+  h->M_max = dicts[0].M;
+  for (auto& d : h->dicts) {
+    h->a_min = std::min(h->a_min, d.a);
+    h->M_max = std::max(h->M_max, d.M);
+  }
+  h->twres = h->M_max;
+  h->Rmax = h->M_max / h->a_min;
+  *out = h;
+  return MPG_OK;
+}
+
+extern "C" void mpgabor_destroy(mpgabor* h) {
+  if (!h) return;
+  if (h->device >= 0) {
+    cudaSetDevice(h->device);
+    for (DevBuf* b : {&h->tw, &h->roots, &h->win, &h->kern, &h->boxcopy, &h->d_pairs, &h->rho, &h->rho_meta,
+                      &h->Hscratch, &h->mxbox, &h->d_geo, &h->grid, &h->rec, &h->xp, &h->partial, &h->flag,
+                      &h->E0, &h->result, &h->sol, &h->frames, &h->hx, &h->hatoms, &h->henergy, &h->hy, &h->prof, &h->d_own})
+      b->release();
+    for (auto e : h->ev)
+      if (e) cudaEventDestroy(e);
+  }
+  delete h;
+}
+
+extern "C" const char* mpgabor_last_error(const mpgabor* h) {
+  return h ? h->err.c_str() : g_create_error.c_str();
+}
+
+// ---------------------------------------------------------------------------
+// kernels (N2)
+// ---------------------------------------------------------------------------
+static int overlap_lags(const mpg_dict& du, const mpg_dict& dv, int a_c, int& nu_lo, int& nu_hi) {
+  const int ju0 = -(du.gl / 2), ju1 = ju0 + du.gl - 1;
+  const int jv0 = -(dv.gl / 2), jv1 = jv0 + dv.gl - 1;
+  nu_lo = (int)-fdiv64(jv1 - ju0, a_c);  // ceil((ju0 - jv1)/a_c)
+  nu_hi = (int)fdiv64(ju1 - jv0, a_c);
+  return nu_hi - nu_lo + 1;
+}
+
+extern "C" int mpgabor_kernels(mpgabor* h, double thr, void* stream) {
+  if (!h) return MPG_EINVAL;
+  if (!(thr >= 0.0 && thr < 1.0)) return h->fail(MPG_EINVAL, "threshold must be in [0, 1)");
+  int rc = enter_device(h);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int W = h->W;
+  h->have_kernels = false;
+  h->thr = thr;
+  // tables
+  TRY_CUDA(h, h->tw.ensure(sizeof(double2) * (h->twres / 2 + 1)));
+  TRY_CUDA(h, h->roots.ensure(sizeof(double2) * h->Rmax));
+  TRY_CUDA(h, launch_tables(h->tw.as<double2>(), h->twres, h->roots.as<double2>(), h->Rmax, st));
+  h->win_off.assign(W + 1, 0);
+  for (int w = 0; w < W; ++w) h->win_off[w + 1] = h->win_off[w] + h->dicts[w].gl;
+  TRY_CUDA(h, h->win.ensure(sizeof(double) * h->win_off[W]));
+  for (int w = 0; w < W; ++w) {
+    const mpg_dict& d = h->dicts[w];
+    TRY_CUDA(h, launch_window(d.win, d.gl, d.a, d.M, h->win.as<double>() + h->win_off[w], st));
+  }
+  // pass 1: per pair lag range, max, box
+  h->pairs.assign(W * W, PairGeo{});
+  h->nu_first.assign(W * W, 0);
+  h->nlag.assign(W * W, 0);
+  h->pair_mx.assign(W * W, 0.0);
+  h->pair_kept.assign(W * W, 0);
+  size_t hmax = 0;
+  for (int u = 0; u < W; ++u)
+    for (int v = 0; v < W; ++v) {
+      const mpg_dict &du = h->dicts[u], &dv = h->dicts[v];
+      PairGeo& pg = h->pairs[u * W + v];
+      pg.a_c = std::min(du.a, dv.a);
+      pg.M_c = std::max(du.M, dv.M);
+      pg.R = pg.M_c / pg.a_c;
+      pg.s_m = pg.M_c / dv.M;
+      pg.s_n = std::max(1, dv.a / pg.a_c);
+      pg.rstep = h->Rmax / pg.R;
+      int lo, hi;
+      const int n = overlap_lags(du, dv, pg.a_c, lo, hi);
+      h->nu_first[u * W + v] = lo;
+      h->nlag[u * W + v] = n;
+      hmax = std::max(hmax, (size_t)n * (pg.M_c / 2 + 1));
+    }
+  TRY_CUDA(h, h->Hscratch.ensure(sizeof(double2) * hmax));
+  TRY_CUDA(h, h->mxbox.ensure(64 * W * W));
+  std::vector<unsigned char> mb(64 * W * W);
+  for (int i = 0; i < W * W; ++i) {
+    unsigned long long z = 0;
+    int box[5] = {INT32_MAX, INT32_MIN, INT32_MAX, INT32_MIN, 0};
+    std::memcpy(&mb[64 * i], &z, 8);
+    std::memcpy(&mb[64 * i + 8], box, sizeof box);
+  }
+  TRY_CUDA(h, cudaMemcpyAsync(h->mxbox.p, mb.data(), mb.size(), cudaMemcpyHostToDevice, st));
+  for (int u = 0; u < W; ++u)
+    for (int v = 0; v < W; ++v) {
+      const int i = u * W + v;
+      const mpg_dict &du = h->dicts[u], &dv = h->dicts[v];
+      PairGeo& pg = h->pairs[i];
+      unsigned char* base = h->mxbox.as<unsigned char>() + 64 * i;
+      TRY_CUDA(h, launch_kern_rows(pg.a_c, pg.M_c, h->nu_first[i], h->nlag[i], h->win.as<double>() + h->win_off[u],
+                                   du.gl, h->win.as<double>() + h->win_off[v], dv.gl, h->tw.as<double2>(), h->twres,
+                                   h->Hscratch.as<double2>(), st));
+      TRY_CUDA(h, launch_kern_max_box(h->Hscratch.as<double2>(), h->nlag[i], pg.M_c, h->nu_first[i], thr,
+                                      reinterpret_cast<unsigned long long*>(base), reinterpret_cast<int*>(base + 8),
+                                      st));
+    }
+  TRY_CUDA(h, cudaMemcpyAsync(mb.data(), h->mxbox.p, mb.size(), cudaMemcpyDeviceToHost, st));
+  TRY_CUDA(h, cudaStreamSynchronize(st));
+  h->kern_elems = 0;
+  h->box_total = 0;
+  h->kept_total = 0;
+  h->box_off.assign(W * W + 1, 0);
+  for (int i = 0; i < W * W; ++i) {
+    unsigned long long mxbits;
+    int box[5];
+    std::memcpy(&mxbits, &mb[64 * i], 8);
+    std::memcpy(box, &mb[64 * i + 8], sizeof box);
+    double mx;
+    std::memcpy(&mx, &mxbits, 8);
+    if (box[0] > box[1]) return h->fail(MPG_ECUDA, "empty kernel box (all-zero kernel)");
+    PairGeo& pg = h->pairs[i];
+    pg.mu_lo = box[0];
+    pg.mu_hi = box[1];
+    pg.nu_lo = box[2];
+    pg.nu_hi = box[3];
+    pg.nmu = box[1] - box[0] + 1;
+    pg.nnu = box[3] - box[2] + 1;
+    pg.koff = h->kern_elems;
+    h->kern_elems += (int64_t)pg.nmu * pg.nnu;
+    h->pair_mx[i] = mx;
+    h->pair_kept[i] = box[4];
+    h->kept_total += box[4];
+    h->box_off[i + 1] = h->box_off[i] + (int64_t)pg.nmu * pg.nnu;
+  }
+  h->box_total = h->kern_elems;
+  // conjugate-pair rows (nu = 0 of h_uu)
+  h->rho_lo.assign(W, 0);
+  h->rho_n.assign(W, 0);
+  h->rho_off.assign(W, 0);
+  h->rho_total = 0;
+  for (int u = 0; u < W; ++u) {
+    const PairGeo& pg = h->pairs[u * W + u];
+    h->rho_off[u] = h->rho_total;
+    h->rho_lo[u] = pg.mu_lo;
+    h->rho_n[u] = (pg.nu_lo <= 0 && pg.nu_hi >= 0) ? pg.nmu : 0;
+    h->rho_total += h->rho_n[u];
+  }
+  TRY_CUDA(h, h->kern.ensure(h->celem() * std::max<int64_t>(1, h->kern_elems)));
+  TRY_CUDA(h, h->boxcopy.ensure(sizeof(double2) * std::max<int64_t>(1, h->box_total)));
+  TRY_CUDA(h, h->rho.ensure(sizeof(RhoEnt) * std::max(1, h->rho_total)));
+  // pass 2: recompute rows and compact
+  for (int u = 0; u < W; ++u)
+    for (int v = 0; v < W; ++v) {
+      const int i = u * W + v;
+      const mpg_dict &du = h->dicts[u], &dv = h->dicts[v];
+      const PairGeo& pg = h->pairs[i];
+      unsigned char* base = h->mxbox.as<unsigned char>() + 64 * i;
+      TRY_CUDA(h, launch_kern_rows(pg.a_c, pg.M_c, h->nu_first[i], h->nlag[i], h->win.as<double>() + h->win_off[u],
+                                   du.gl, h->win.as<double>() + h->win_off[v], dv.gl, h->tw.as<double2>(), h->twres,
+                                   h->Hscratch.as<double2>(), st));
+      RhoEnt* rrow = (u == v && h->rho_n[u] > 0) ? h->rho.as<RhoEnt>() + h->rho_off[u] : nullptr;
+      if (h->f64())
+        TRY_CUDA(h, launch_kern_compact<double>(h->Hscratch.as<double2>(), pg.M_c, h->nu_first[i], thr,
+                                                reinterpret_cast<const unsigned long long*>(base), pg,
+                                                h->kern.as<double2>(), h->boxcopy.as<double2>() + h->box_off[i],
+                                                rrow, st));
+      else
+        TRY_CUDA(h, launch_kern_compact<float>(h->Hscratch.as<double2>(), pg.M_c, h->nu_first[i], thr,
+                                               reinterpret_cast<const unsigned long long*>(base), pg,
+                                               h->kern.as<float2>(), h->boxcopy.as<double2>() + h->box_off[i], rrow,
+                                               st));
+    }
+  TRY_CUDA(h, h->d_pairs.ensure(sizeof(PairGeo) * W * W));
+  TRY_CUDA(h, cudaMemcpyAsync(h->d_pairs.p, h->pairs.data(), sizeof(PairGeo) * W * W, cudaMemcpyHostToDevice, st));
+  std::vector<int> meta(3 * W);
+  for (int u = 0; u < W; ++u) {
+    meta[u] = h->rho_lo[u];
+    meta[W + u] = h->rho_n[u];
+    meta[2 * W + u] = h->rho_off[u];
+  }
+  TRY_CUDA(h, h->rho_meta.ensure(sizeof(int) * 3 * W));
+  TRY_CUDA(h, cudaMemcpyAsync(h->rho_meta.p, meta.data(), sizeof(int) * 3 * W, cudaMemcpyHostToDevice, st));
+  TRY_CUDA(h, cudaStreamSynchronize(st));
+  h->Hscratch.release();
+  h->have_kernels = true;
+  h->L = -1;  // layout depends on kernel boxes (validation), recompute at next run
+  return MPG_OK;
+}
+
+extern "C" int mpgabor_kernel_stats(const mpgabor* h, int64_t* box_entries, int64_t* kept_entries, int64_t* bytes) {
+  if (!h) return MPG_EINVAL;
+  if (!h->have_kernels) return const_cast<mpgabor*>(h)->fail(MPG_ESTATE, "kernels not computed");
+  if (box_entries) *box_entries = h->box_total;
+  if (kept_entries) *kept_entries = h->kept_total;
+  if (bytes) *bytes = h->kern_elems * (int64_t)h->celem();
+  return MPG_OK;
+}
+
+extern "C" int mpgabor_kernel_box(mpgabor* h, int32_t u, int32_t v, int32_t* box, double* values, double* mx) {
+  if (!h || !box) return MPG_EINVAL;
+  if (!h->have_kernels) return h->fail(MPG_ESTATE, "kernels not computed");
+  if (u < 0 || v < 0 || u >= h->W || v >= h->W) return h->fail(MPG_EINVAL, "pair index out of range");
+  const PairGeo& pg = h->pairs[u * h->W + v];
+  box[0] = pg.mu_lo;
+  box[1] = pg.mu_hi;
+  box[2] = pg.nu_lo;
+  box[3] = pg.nu_hi;
+  if (mx) *mx = h->pair_mx[u * h->W + v];
+  if (values) {
+    int rc = enter_device(h);
+    if (rc) return rc;
+    TRY_CUDA(h, cudaMemcpy(values, h->boxcopy.as<double2>() + h->box_off[u * h->W + v],
+                           sizeof(double2) * pg.nmu * pg.nnu, cudaMemcpyDeviceToHost));
+  }
+  return MPG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// layout
+// ---------------------------------------------------------------------------
+static int64_t ell_of(const mpgabor* h) {
+  int64_t ell = 1;
+  for (auto& d : h->dicts) {
+    ell = std::lcm(ell, (int64_t)d.a);
+    ell = std::lcm(ell, (int64_t)d.M);
+  }
+  return ell;
+}
+
+extern "C" int mpgabor_layout(const mpgabor* h, int64_t Ls, int64_t* L_pad, int64_t* N, int64_t* M_R,
+                              int64_t* coef_offset) {
+  if (!h) return MPG_EINVAL;
+  if (Ls < 1) return const_cast<mpgabor*>(h)->fail(MPG_EINVAL, "Ls must be >= 1");
+  const int64_t ell = ell_of(h);
+  if (Ls > (int64_t)1 << 40) return const_cast<mpgabor*>(h)->fail(MPG_ELEN, "Ls too large");
+  const int64_t L = (Ls + ell - 1) / ell * ell;
+  if (L_pad) *L_pad = L;
+  int64_t off = 0;
+  for (int w = 0; w < h->W; ++w) {
+    const int64_t n = L / h->dicts[w].a, mr = h->dicts[w].M / 2 + 1;
+    if (N) N[w] = n;
+    if (M_R) M_R[w] = mr;
+    if (coef_offset) coef_offset[w] = off;
+    off += n * mr;
+  }
+  if (coef_offset) coef_offset[h->W] = off;
+  return MPG_OK;
+}
+
+extern "C" int mpgabor_set_launch(mpgabor* h, int32_t cluster, int32_t threads, int32_t tile_width,
+                                  int32_t records) {
+  if (!h) return MPG_EINVAL;
+  if (cluster < 0 || cluster > 16 || (cluster && (cluster & (cluster - 1))))
+    return h->fail(MPG_EINVAL, "cluster must be 0 or a power of two <= 16");
+  if (threads && (threads < 128 || threads > 512 || threads % 32))
+    return h->fail(MPG_EINVAL, "threads must be in [128,512], multiple of 32");
+  if (tile_width && tile_width != 32 && tile_width != 64 && tile_width != 128)
+    return h->fail(MPG_EINVAL, "tile width must be 32, 64 or 128");
+  if (records < 0 || records > 2) return h->fail(MPG_EINVAL, "records must be 0 (auto), 1 (shared) or 2 (global)");
+  h->cluster_req = cluster;
+  if (threads) h->threads = threads;
+  h->TW_req = tile_width;
+  h->srec_req = records;
+  h->L = -1;
+  return MPG_OK;
+}
+
+// grids and tiles of every dictionary for tile width TW (fills h->geo, sizes)
+static int plan_grids(mpgabor* h, int64_t L, int TW) {
+  const int W = h->W;
+  h->geo.assign(W, DictGeo{});
+  int64_t off = 0, goff = 0, toff = 0, foff = 0;
+  for (int w = 0; w < W; ++w) {
+    DictGeo& d = h->geo[w];
+    const mpg_dict& s = h->dicts[w];
+    d.win = s.win;
+    d.gl = s.gl;
+    d.a = s.a;
+    d.M = s.M;
+    d.N = (int32_t)(L / s.a);
+    d.frame_off = (int32_t)foff;
+    foff += d.N;
+    d.MR = s.M / 2 + 1;
+    d.T = (d.MR + TW - 1) / TW;
+    d.stride = d.T * TW;
+    d.off = off;
+    d.grid_off = goff;
+    d.tile_off = toff;
+    off += (int64_t)d.N * d.MR;
+    goff += (int64_t)d.N * d.stride;
+    toff += (int64_t)d.N * d.T;
+  }
+  h->P_R = off;
+  h->grid_elems = goff;
+  h->total_tiles = toff;
+  if (h->P_R >= (int64_t)NO_INDEX || h->total_tiles > INT32_MAX)
+    return h->fail(MPG_ELEN, "more than 2^32-1 reduced coefficients");
+  return MPG_OK;
+}
+
+// loop parameters for (TW, srec, C); returns shared-memory bytes (SIZE_MAX if the tree is too deep)
+static size_t plan_loop(mpgabor* h, int TW, int srec, int C) {
+  LoopParams& P = h->lp;
+  P = LoopParams{};
+  P.W = h->W;
+  P.TW = TW;
+  P.srec = srec;
+  P.Rmax = h->Rmax;
+  P.rho_total = h->rho_total;
+  P.C = C;
+  // frame ownership: global frame f -> CTA f mod C; per (CTA, dictionary) first owned
+  // frame, owned-frame count and the local index of the first tile record
+  h->own.assign((size_t)C * h->W, OwnGeo{});
+  int64_t Lc = 0;
+  for (int c = 0; c < C; ++c) {
+    int64_t loc = 0;
+    for (int v = 0; v < h->W; ++v) {
+      const DictGeo& d = h->geo[v];
+      OwnGeo& o = h->own[(size_t)c * h->W + v];
+      o.n_first = (int32_t)(((c - d.frame_off) % C + C) % C);
+      o.n_own = o.n_first < d.N ? (d.N - 1 - o.n_first) / C + 1 : 0;
+      o.loc_base = (int32_t)loc;
+      loc += (int64_t)o.n_own * d.T;
+    }
+    Lc = std::max(Lc, loc);
+  }
+  P.Lc = Lc;
+  int n = (int)((P.Lc + 31) / 32), nl = 0, o = 0;
+  for (;;) {
+    if (nl >= MAX_LEVELS) return SIZE_MAX;
+    P.lev_n[nl] = n;
+    P.lev_off[nl] = o;
+    o += n;
+    ++nl;
+    if (n <= TOP_SCAN) break;
+    n = (n + 31) / 32;
+  }
+  P.nlev = nl;
+  P.smem_bytes = loop_smem_bytes(P, h->f64());
+  return P.smem_bytes;
+}
+
+static int ensure_layout(mpgabor* h, int64_t Ls) {
+  const int64_t ell = ell_of(h);
+  const int64_t L = (Ls + ell - 1) / ell * ell;
+  if (L == h->L) return MPG_OK;
+  const int W = h->W;
+  if (L > ((int64_t)1 << 30)) return h->fail(MPG_ELEN, "L_pad larger than 2^30");
+  // aliasing / box checks (circular Gram == direct overlap needs L >= gl_u + gl_v)
+  for (int u = 0; u < W; ++u)
+    for (int v = 0; v < W; ++v) {
+      const PairGeo& pg = h->pairs[u * W + v];
+      if (L < (int64_t)h->dicts[u].gl + h->dicts[v].gl)
+        return h->fail(MPG_ELEN, "L_pad shorter than gl_u + gl_v (kernel would alias circularly)");
+      const int rows = (pg.nnu + pg.s_n - 1) / pg.s_n, cols = (pg.nmu + pg.s_m - 1) / pg.s_m;
+      if (rows > L / h->dicts[v].a || cols > h->dicts[v].M)
+        return h->fail(MPG_ELEN, "kernel box wider than the target grid");
+    }
+  // candidate launch plans, first schedulable wins
+  struct Cand { int TW, srec; };
+  std::vector<Cand> cands;
+  const int tws[2] = {h->TW_req ? h->TW_req : 64, h->TW_req ? h->TW_req : 128};
+  if (h->srec_req != 2) {
+    cands.push_back({tws[0], 1});
+    if (tws[1] != tws[0]) cands.push_back({tws[1], 1});
+  }
+  if (h->srec_req != 1) cands.push_back({tws[0], 0});
+  std::string why = "no candidate";
+  bool ok = false;
+  for (const Cand& c : cands) {
+    int rc = plan_grids(h, L, c.TW);
+    if (rc) return rc;
+    for (int C = h->cluster_req ? h->cluster_req : MAX_CLUSTER; C >= 1; C >>= 1) {
+      const size_t smem = plan_loop(h, c.TW, c.srec, C);
+      if (smem > 227 * 1024) {
+        why = "shared memory " + std::to_string(smem) + " B";
+        break;  // smaller clusters need more per-CTA memory
+      }
+      const int cmax = loop_max_cluster(h->f64(), c.srec, c.TW, h->threads, smem);
+      if (cmax >= C) {
+        ok = true;
+        break;
+      }
+      why = "cluster of " + std::to_string(C) + " not schedulable";
+      if (h->cluster_req) break;
+    }
+    if (ok) {
+      h->TW = c.TW;
+      h->srec = c.srec;
+      break;
+    }
+  }
+  if (!ok) return h->fail(MPG_ECUDA, "no launch plan for the MP loop: " + why);
+  LoopParams& P = h->lp;
+  h->lay_C = P.C;
+  // buffers
+  TRY_CUDA(h, h->d_geo.ensure(sizeof(DictGeo) * W));
+  TRY_CUDA(h, cudaMemcpy(h->d_geo.p, h->geo.data(), sizeof(DictGeo) * W, cudaMemcpyHostToDevice));
+  TRY_CUDA(h, h->d_own.ensure(sizeof(OwnGeo) * h->own.size()));
+  TRY_CUDA(h, cudaMemcpy(h->d_own.p, h->own.data(), sizeof(OwnGeo) * h->own.size(), cudaMemcpyHostToDevice));
+  TRY_CUDA(h, h->grid.ensure(h->celem() * h->grid_elems));
+  TRY_CUDA(h, h->rec.ensure((h->f64() ? sizeof(Rec<double>) : sizeof(Rec<float>)) * P.C * P.Lc));
+  TRY_CUDA(h, h->xp.ensure(sizeof(double) * L));
+  TRY_CUDA(h, h->partial.ensure(sizeof(double) * 256));
+  TRY_CUDA(h, h->flag.ensure(sizeof(int)));
+  TRY_CUDA(h, h->E0.ensure(sizeof(double)));
+  TRY_CUDA(h, h->result.ensure(sizeof(LoopResult)));
+  h->L = L;
+  h->lay_TW = h->TW;
+  return MPG_OK;
+}
+
+extern "C" int mpgabor_launch_info(const mpgabor* h, int32_t* cluster, int32_t* threads, int32_t* tile_width,
+                                   int32_t* records, int64_t* smem_bytes) {
+  if (!h) return MPG_EINVAL;
+  if (h->L < 0) return const_cast<mpgabor*>(h)->fail(MPG_ESTATE, "no run yet");
+  if (cluster) *cluster = h->lp.C;
+  if (threads) *threads = h->threads;
+  if (tile_width) *tile_width = h->TW;
+  if (records) *records = h->srec ? 1 : 2;
+  if (smem_bytes) *smem_bytes = (int64_t)h->lp.smem_bytes;
+  return MPG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// run
+// ---------------------------------------------------------------------------
+extern "C" int mpgabor_run(mpgabor* h, const double* x_dev, int64_t Ls, int64_t maxit, double errdb,
+                           mpg_atom* atoms_dev, double* energy_dev, double* coef_dev, mpg_result* res,
+                           void* stream) {
+  if (!h) return MPG_EINVAL;
+  if (!x_dev || !energy_dev || !res || (maxit > 0 && !atoms_dev)) return h->fail(MPG_EINVAL, "null pointer");
+  if (Ls < 1) return h->fail(MPG_EINVAL, "Ls must be >= 1");
+  if (maxit < 0) return h->fail(MPG_EINVAL, "maxit must be >= 0");
+  if (std::isnan(errdb)) return h->fail(MPG_EINVAL, "errdb is NaN");
+  if (!h->have_kernels) return h->fail(MPG_ESTATE, "mpgabor_kernels must run before mpgabor_run");
+  int rc = enter_device(h);
+  if (rc) return rc;
+  rc = ensure_layout(h, Ls);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int W = h->W;
+  TRY_CUDA(h, cudaEventRecord(h->ev[0], st));
+  TRY_CUDA(h, cudaMemsetAsync(h->flag.p, 0, sizeof(int), st));
+  TRY_CUDA(h, launch_pad_energy(x_dev, Ls, h->xp.as<double>(), h->L, h->partial.as<double>(), h->flag.as<int>(),
+                                h->E0.as<double>(), st));
+  for (int w = 0; w < W; ++w) {
+    const DictGeo& d = h->geo[w];
+    const double* g = h->win.as<double>() + h->win_off[w];
+    if (h->f64())
+      TRY_CUDA(h, launch_dgt<double>(h->xp.as<double>(), h->L, d, g, h->tw.as<double2>(), h->twres,
+                                     h->grid.as<double2>() + d.grid_off, st));
+    else
+      TRY_CUDA(h, launch_dgt<float>(h->xp.as<double>(), h->L, d, g, h->tw.as<double2>(), h->twres,
+                                    h->grid.as<float2>() + d.grid_off, st));
+  }
+  TRY_CUDA(h, cudaEventRecord(h->ev[1], st));
+  LoopParams& P = h->lp;
+  if (h->f64())
+    TRY_CUDA(h, launch_tile_init<double>(h->grid.as<double2>(), h->d_geo.as<DictGeo>(), h->d_own.as<OwnGeo>(), W, h->total_tiles, P.C, P.Lc,
+                                         h->TW, h->rec.as<Rec<double>>(), st));
+  else
+    TRY_CUDA(h, launch_tile_init<float>(h->grid.as<float2>(), h->d_geo.as<DictGeo>(), h->d_own.as<OwnGeo>(), W, h->total_tiles, P.C, P.Lc,
+                                        h->TW, h->rec.as<Rec<float>>(), st));
+  if (coef_dev) TRY_CUDA(h, cudaMemsetAsync(coef_dev, 0, sizeof(double2) * h->P_R, st));
+  TRY_CUDA(h, cudaMemcpyAsync(energy_dev, h->E0.p, sizeof(double), cudaMemcpyDeviceToDevice, st));
+  TRY_CUDA(h, cudaEventRecord(h->ev[2], st));
+  double E0 = 0.0;
+  int nonfinite = 0;
+  TRY_CUDA(h, cudaMemcpyAsync(&E0, h->E0.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+  TRY_CUDA(h, cudaMemcpyAsync(&nonfinite, h->flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  TRY_CUDA(h, cudaStreamSynchronize(st));
+  if (nonfinite) return h->fail(MPG_ENONFINITE, "x contains NaN or Inf");
+  // stop level 10^(errdb/10) E_0
+  const double Etol = (errdb == -INFINITY) ? -INFINITY : std::pow(10.0, errdb / 10.0) * E0;
+  P.dicts = h->d_geo.as<DictGeo>();
+  P.own = h->d_own.as<OwnGeo>();
+  P.pairs = h->d_pairs.as<PairGeo>();
+  P.roots = h->roots.as<double2>();
+  P.rho = h->rho.as<RhoEnt>();
+  P.rho_lo = h->rho_meta.as<int>();
+  P.rho_n = h->rho_meta.as<int>() + W;
+  P.rho_off = h->rho_meta.as<int>() + 2 * W;
+  P.grid = h->grid.p;
+  P.kern = h->kern.p;
+  P.rec = h->rec.p;
+  P.maxit = maxit;
+  P.Etol = Etol;
+  P.E0 = E0;
+  P.atoms = reinterpret_cast<AtomOut*>(atoms_dev);
+  P.energy = energy_dev;
+  P.sol = reinterpret_cast<double2*>(coef_dev);
+  P.result = h->result.as<LoopResult>();
+  P.floor_mode = (h->prof_mode & 2) ? 1 : 0;
+  P.prof = nullptr;
+  if (h->prof_mode & 1) {
+    TRY_CUDA(h, h->prof.ensure(sizeof(long long) * 8));
+    TRY_CUDA(h, cudaMemsetAsync(h->prof.p, 0, sizeof(long long) * 8, st));
+    P.prof = h->prof.as<long long>();
+  }
+  TRY_CUDA(h, cudaEventRecord(h->ev[3], st));
+  TRY_CUDA(h, launch_mp_loop(P, h->f64(), h->threads, st));
+  TRY_CUDA(h, cudaEventRecord(h->ev[4], st));
+  LoopResult lr{};
+  TRY_CUDA(h, cudaMemcpyAsync(&lr, h->result.p, sizeof lr, cudaMemcpyDeviceToHost, st));
+  TRY_CUDA(h, cudaStreamSynchronize(st));
+  TRY_CUDA(h, cudaEventElapsedTime(&h->t_dgt, h->ev[0], h->ev[1]));
+  TRY_CUDA(h, cudaEventElapsedTime(&h->t_init, h->ev[1], h->ev[2]));
+  TRY_CUDA(h, cudaEventElapsedTime(&h->t_loop, h->ev[3], h->ev[4]));
+  if (P.prof) TRY_CUDA(h, cudaMemcpy(h->prof_host, P.prof, sizeof(long long) * 8, cudaMemcpyDeviceToHost));
+  res->n_atoms = lr.n_done;
+  res->L_pad = h->L;
+  res->stop_reason = lr.stop;
+  res->cluster = h->lay_C;
+  res->E0 = E0;
+  res->E_final = lr.E_final;
+  return MPG_OK;
+}
+
+extern "C" int mpgabor_set_profile(mpgabor* h, int32_t mode) {
+  if (!h) return MPG_EINVAL;
+  if (mode < 0 || mode > 3) return h->fail(MPG_EINVAL, "profile mode must be in [0, 3]");
+  h->prof_mode = mode;
+  return MPG_OK;
+}
+
+extern "C" int mpgabor_last_profile(const mpgabor* h, int64_t* cycles) {
+  if (!h || !cycles) return MPG_EINVAL;
+  for (int i = 0; i < 8; ++i) cycles[i] = h->prof_host[i];
+  return MPG_OK;
+}
+
+extern "C" int mpgabor_last_timing(const mpgabor* h, double* dgt_ms, double* init_ms, double* loop_ms) {
+  if (!h) return MPG_EINVAL;
+  if (dgt_ms) *dgt_ms = h->t_dgt;
+  if (init_ms) *init_ms = h->t_init;
+  if (loop_ms) *loop_ms = h->t_loop;
+  return MPG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// synthesis
+// ---------------------------------------------------------------------------
+extern "C" int mpgabor_synth(mpgabor* h, const mpg_atom* atoms_dev, int64_t n_atoms, double* y_dev, int64_t Ls,
+                             void* stream) {
+  if (!h) return MPG_EINVAL;
+  if (!y_dev || (n_atoms > 0 && !atoms_dev)) return h->fail(MPG_EINVAL, "null pointer");
+  if (Ls < 1 || n_atoms < 0) return h->fail(MPG_EINVAL, "Ls must be >= 1 and n_atoms >= 0");
+  if (!h->have_kernels) return h->fail(MPG_ESTATE, "mpgabor_kernels must run before mpgabor_synth");
+  int rc = enter_device(h);
+  if (rc) return rc;
+  rc = ensure_layout(h, Ls);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  TRY_CUDA(h, h->sol.ensure(sizeof(double2) * h->P_R));
+  int64_t fmax = 0;
+  for (auto& d : h->geo) fmax = std::max(fmax, (int64_t)d.N * d.M);
+  TRY_CUDA(h, h->frames.ensure(sizeof(double) * fmax));
+  TRY_CUDA(h, cudaMemsetAsync(h->sol.p, 0, sizeof(double2) * h->P_R, st));
+  TRY_CUDA(h, launch_synth_scatter(reinterpret_cast<const AtomOut*>(atoms_dev), n_atoms, h->d_geo.as<DictGeo>(), h->W,
+                                   h->sol.as<double2>(), st));
+  for (int w = 0; w < h->W; ++w) {
+    const DictGeo& d = h->geo[w];
+    TRY_CUDA(h, launch_synth_frames(h->sol.as<double2>(), d, h->tw.as<double2>(), h->twres, h->frames.as<double>(), st));
+    TRY_CUDA(h, launch_synth_ola(h->frames.as<double>(), d, h->win.as<double>() + h->win_off[w], Ls, y_dev, w > 0, st));
+  }
+  return MPG_OK;
+}
+
+extern "C" int mpgabor_decompose_host(mpgabor* h, const double* x_host, int64_t Ls, int64_t maxit, double errdb,
+                                      mpg_atom* atoms_host, double* energy_host, double* y_host, mpg_result* res,
+                                      void* stream) {
+  if (!h) return MPG_EINVAL;
+  if (!x_host || !res) return h->fail(MPG_EINVAL, "null pointer");
+  if (Ls < 1 || maxit < 0) return h->fail(MPG_EINVAL, "Ls must be >= 1 and maxit >= 0");
+  int rc = enter_device(h);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  TRY_CUDA(h, h->hx.ensure(sizeof(double) * Ls));
+  TRY_CUDA(h, h->hatoms.ensure(sizeof(mpg_atom) * std::max<int64_t>(1, maxit)));
+  TRY_CUDA(h, h->henergy.ensure(sizeof(double) * (maxit + 1)));
+  TRY_CUDA(h, h->hy.ensure(sizeof(double) * Ls));
+  TRY_CUDA(h, cudaMemcpyAsync(h->hx.p, x_host, sizeof(double) * Ls, cudaMemcpyHostToDevice, st));
+  rc = mpgabor_run(h, h->hx.as<double>(), Ls, maxit, errdb, h->hatoms.as<mpg_atom>(), h->henergy.as<double>(), nullptr,
+                   res, stream);
+  if (rc) return rc;
+  if (y_host) {
+    rc = mpgabor_synth(h, h->hatoms.as<mpg_atom>(), res->n_atoms, h->hy.as<double>(), Ls, stream);
+    if (rc) return rc;
+    TRY_CUDA(h, cudaMemcpyAsync(y_host, h->hy.p, sizeof(double) * Ls, cudaMemcpyDeviceToHost, st));
+  }
+  if (atoms_host && res->n_atoms > 0)
+    TRY_CUDA(h, cudaMemcpyAsync(atoms_host, h->hatoms.p, sizeof(mpg_atom) * res->n_atoms, cudaMemcpyDeviceToHost, st));
+  if (energy_host)
+    TRY_CUDA(h, cudaMemcpyAsync(energy_host, h->henergy.p, sizeof(double) * (res->n_atoms + 1),
+                                cudaMemcpyDeviceToHost, st));
+  TRY_CUDA(h, cudaStreamSynchronize(st));
+  return MPG_OK;
+}

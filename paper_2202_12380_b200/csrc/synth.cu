@@ -1,0 +1,112 @@
+// synth.cu -- N6: synthesis of the approximation from an atom list (Eq. (18)):
+//   y = sum_atoms c~ d (self-conjugate m = 0, M/2) or 2 Re(c~ d) (pairs).
+// The atoms are first scattered into a solution grid (complex, unpadded), then
+// every frame is inverted with one half-length complex IFFT in shared memory
+// (c2r with Hermitian extension, X[M-m] = conj X[m]) and the windowed frames are
+// overlap-added by a gather over output samples (fixed order -> deterministic).
+#include <algorithm>
+#include "launch.h"
+#include "fft.cuh"
+
+__global__ void synth_scatter_kernel(const AtomOut* __restrict__ atoms, int64_t n, const DictGeo* __restrict__ dg,
+                                     double2* __restrict__ sol) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const AtomOut a = atoms[i];
+    const DictGeo d = dg[a.w];
+    double* s = reinterpret_cast<double*>(sol + d.off + (int64_t)a.n * d.MR + a.m);
+    atomicAdd(s, a.re);
+    if (a.im != 0.0) atomicAdd(s + 1, a.im);
+  }
+}
+
+// frame n: t[s] = sum_{m=0}^{M-1} X[m] e^{+2 pi i m s/M}, X[0], X[M/2] real parts,
+// X[M-m] = conj X[m]; via Z[m] = A[m] + i B[m], A = X[m] + conj X[n-m],
+// B = (X[m] - conj X[n-m]) e^{+2 pi i m/M}, z = IFFT_n(Z), t[2r] = Re z[r], t[2r+1] = Im z[r].
+__global__ void synth_frames_kernel(const double2* __restrict__ sol, int64_t off, int M, int MR, int N,
+                                    const double2* __restrict__ tw, int twres, double* __restrict__ frames, int F) {
+  extern __shared__ double2 z[];
+  const int n = M / 2;
+  const int lgn = 31 - __clz(n);
+  const int frame0 = blockIdx.x * F;
+  for (int idx = threadIdx.x; idx < F * n; idx += blockDim.x) {
+    const int f = idx / n, m = idx - f * n;
+    const int frame = frame0 + f;
+    double2 Zm = make_double2(0.0, 0.0);
+    if (frame < N) {
+      const double2* X = sol + off + (int64_t)frame * MR;
+      double2 a = X[m];
+      double2 b = X[n - m];
+      if (m == 0) {
+        a.y = 0.0;
+        b.y = 0.0;
+      }
+      const double2 bc = cconj(b);
+      const double2 A = cadd(a, bc);
+      double2 wp = __ldg(&tw[(int64_t)m * (twres / M)]);
+      wp.y = -wp.y;  // e^{+2 pi i m/M}
+      const double2 B = cmul(csub(a, bc), wp);
+      Zm = make_double2(A.x - B.y, A.y + B.x);  // A + iB
+    }
+    z[f * n + bitrev(m, lgn)] = Zm;
+  }
+  __syncthreads();
+  smem_fft(z, lgn, F, tw, twres, +1);
+  for (int idx = threadIdx.x; idx < F * n; idx += blockDim.x) {
+    const int f = idx / n, r = idx - f * n;
+    const int frame = frame0 + f;
+    if (frame >= N) continue;
+    const double2 v = z[f * n + r];
+    frames[(int64_t)frame * M + 2 * r] = v.x;
+    frames[(int64_t)frame * M + 2 * r + 1] = v.y;
+  }
+}
+
+// y[l] (+)= sum over frames nn covering l, ascending: g(j) t_nn(j mod M), j = l - nn a
+__global__ void synth_ola_kernel(const double* __restrict__ frames, int a, int M, int N, int gl,
+                                 const double* __restrict__ g, int64_t L, int64_t Ls, double* __restrict__ y,
+                                 int accumulate) {
+  const int j0 = -(gl / 2), j1 = j0 + gl - 1;
+  for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < Ls; l += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t nlo = -fdiv64(-(l - j1), a);  // ceil((l - j1)/a)
+    const int64_t nhi = fdiv64(l - j0, a);
+    double acc = 0.0;
+    for (int64_t nn = nlo; nn <= nhi; ++nn) {
+      const int64_t j = l - nn * a;
+      const int64_t fr = fmod64(nn, N);
+      acc += g[j - j0] * frames[fr * M + fmod64(j, M)];
+    }
+    y[l] = accumulate ? y[l] + acc : acc;
+  }
+  (void)L;
+}
+
+cudaError_t launch_synth_scatter(const AtomOut* atoms, int64_t n_atoms, const DictGeo* dg_dev, int W, double2* sol,
+                                 cudaStream_t st) {
+  (void)W;
+  if (n_atoms <= 0) return cudaSuccess;
+  const int blocks = (int)std::min<int64_t>(1184, (n_atoms + 255) / 256);
+  synth_scatter_kernel<<<blocks, 256, 0, st>>>(atoms, n_atoms, dg_dev, sol);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_synth_frames(const double2* sol, const DictGeo& d, const double2* tw, int twres, double* frames,
+                                cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    CUDA_OK(cudaFuncSetAttribute(synth_frames_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr = true;
+  }
+  const int n = d.M / 2;
+  const int F = max(1, 2048 / n);
+  synth_frames_kernel<<<(d.N + F - 1) / F, 256, (size_t)F * n * sizeof(double2), st>>>(sol, d.off, d.M, d.MR, d.N,
+                                                                                       tw, twres, frames, F);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_synth_ola(const double* frames, const DictGeo& d, const double* g, int64_t L, double* y,
+                             int accumulate, cudaStream_t st) {
+  // y has Ls = L entries here (caller passes the truncated length as L)
+  const int blocks = (int)std::min<int64_t>(148 * 16, (L + 255) / 256);
+  synth_ola_kernel<<<blocks, 256, 0, st>>>(frames, d.a, d.M, d.N, d.gl, g, L, L, y, accumulate);
+  return cudaGetLastError();
+}
