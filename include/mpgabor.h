@@ -176,6 +176,15 @@ int mpgabor_kernel_box(mpgabor* h, int32_t u, int32_t v, int32_t* box, double* v
  * NULL): analysis (pad + energy + DGT), max-structure init, iteration loop. */
 int mpgabor_last_timing(const mpgabor* h, double* dgt_ms, double* init_ms, double* loop_ms);
 
+/* Number of this library's CUDA kernels enqueued through h so far (host output). */
+int mpgabor_launch_count(const mpgabor* h, int64_t* n);
+
+/* Copy the coefficient-domain residual c^ of the last mpgabor_run (after its
+ * final selection; after the DGT alone when maxit = 0) to out_dev (device
+ * complex double[P_R], interleaved, index p as in mpgabor_layout), converting
+ * from the run precision.  For tests and diagnostics.  Synchronises cuda_stream. */
+int mpgabor_residual(mpgabor* h, double* out_dev, void* cuda_stream);
+
 /* Instrumentation of the persistent loop (takes effect at the next run):
  * mode bit0 = accumulate per-phase SM clock cycles on CTA 0 / thread 0;
  * mode bit1 = latency-floor mode: the residual update is skipped (selection,

@@ -211,6 +211,67 @@ def synthesize(atoms, dicts, L, Ls=None):
 
 
 # ---------------------------------------------------------------------------
+# Residual at single coefficients, one by one: c^_K(p) = c^_0(p) - sum_k (update
+# of atom k at p).  The update of atom k = (u, k, j, c~) at target p = (v, m, n) is
+# Alg. 3 restricted to one target: with a_c, M_c of the pair, the
+# time lag nu = (n a_v - j a_u)/a_c (circular, signed) and the modulation
+# omega_R^{(k' nu) mod R} (Eq. (15)),
+#   direct:   - c~ omega h(m s_m - k', nu)
+#   conj:     - conj(c~ omega h(((M_v - m) mod M_v) s_m - k', nu))   (pair atoms, Z14)
+# (mu reduced to the signed range, h = 0 outside the kept box).
+# ---------------------------------------------------------------------------
+def residual_at(setup, atoms, points):
+    """points: int array of global indices p; returns complex128 c^_K(p)."""
+    lay, dicts, W = setup.lay, setup.dicts, len(setup.dicts)
+    L = lay.L
+    res0 = np.concatenate([g.ravel() for g in setup.grids])
+    out = np.empty(len(points), dtype=np.complex128)
+    aw = np.asarray(atoms["w"])
+    am = np.asarray(atoms["m"]).astype(np.int64)
+    an = np.asarray(atoms["n"]).astype(np.int64)
+    ac = np.asarray(atoms["re"]) + 1j * np.asarray(atoms["im"])
+    aself = (np.asarray(atoms["flags"]) & 1) == 1
+    for i, p in enumerate(np.asarray(points, dtype=np.int64)):
+        v = int(np.searchsorted(lay.off, p, side="right") - 1)
+        n, m = divmod(int(p - lay.off[v]), lay.MR[v])
+        dv = dicts[v]
+        acc = complex(res0[p])
+        for u in range(W):
+            sel = np.nonzero(aw == u)[0]
+            if sel.size == 0:
+                continue
+            K = setup.K[u * W + v]
+            du = dicts[u]
+            a_c, M_c = K.a_c, K.M_c
+            R = M_c // a_c
+            s_m = M_c // dv.M
+            kp = am[sel] * (M_c // du.M)
+            dt = (n * dv.a - an[sel] * du.a) % L
+            dt = np.where(dt > L // 2, dt - L, dt)
+            nu = dt // a_c
+            inb = (nu >= K.nu_lo) & (nu <= K.nu_hi)
+            if not inb.any():
+                continue
+            sel, kp, nu = sel[inb], kp[inb], nu[inb]
+            omega = np.exp(2j * np.pi * ((kp * nu) % R) / R)
+
+            def hval(mu):
+                mu = mu % M_c
+                mu = np.where(2 * mu > M_c, mu - M_c, mu)
+                ok = (mu >= K.mu_lo) & (mu <= K.mu_hi)
+                vals = np.zeros(mu.shape, dtype=np.complex128)
+                vals[ok] = K.h[nu[ok] - K.nu_lo, mu[ok] - K.mu_lo]
+                return vals
+
+            zd = ac[sel] * omega * hval(m * s_m - kp)
+            zc = ac[sel] * omega * hval(((dv.M - m) % dv.M) * s_m - kp)
+            contrib = zd + np.where(aself[sel], 0.0, np.conj(zc))
+            acc -= contrib.sum()
+        out[i] = acc
+    return out
+
+
+# ---------------------------------------------------------------------------
 # O6 initial state bundle
 # ---------------------------------------------------------------------------
 @dataclass

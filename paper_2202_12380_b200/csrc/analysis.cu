@@ -312,6 +312,22 @@ __global__ void rec_clear_kernel(Rec<R>* __restrict__ rec, int64_t n) {
     rec[i] = empty_rec(R(0));
 }
 
+// residual export: padded grid (cplx<R>) -> complex double in global index order p
+template <typename R>
+__global__ void grid_export_kernel(const typename cplx<R>::t* __restrict__ grid, const DictGeo* __restrict__ dg,
+                                   int W, int64_t P, double2* __restrict__ out) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P; p += (int64_t)gridDim.x * blockDim.x) {
+    int v = 0;
+    while (v + 1 < W && dg[v + 1].off <= p) ++v;
+    const DictGeo d = dg[v];
+    const int64_t q = p - d.off;
+    const int64_t n = q / d.MR;
+    const int64_t m = q - n * d.MR;
+    const typename cplx<R>::t c = grid[d.grid_off + n * d.stride + m];
+    out[p] = make_double2((double)c.x, (double)c.y);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
@@ -402,6 +418,15 @@ cudaError_t launch_tile_init(const typename cplx<R>::t* grid, const DictGeo* dg,
   }
   return cudaGetLastError();
 }
+template <typename R>
+cudaError_t launch_grid_export(const typename cplx<R>::t* grid, const DictGeo* dg, int W, int64_t P, double2* out,
+                               cudaStream_t st) {
+  grid_export_kernel<R><<<(int)std::min<int64_t>(1184, (P + 255) / 256), 256, 0, st>>>(grid, dg, W, P, out);
+  return cudaGetLastError();
+}
+template cudaError_t launch_grid_export<double>(const double2*, const DictGeo*, int, int64_t, double2*, cudaStream_t);
+template cudaError_t launch_grid_export<float>(const float2*, const DictGeo*, int, int64_t, double2*, cudaStream_t);
+
 template cudaError_t launch_tile_init<double>(const double2*, const DictGeo*, const OwnGeo*, int, int64_t, int,
                                               int64_t, int, Rec<double>*, cudaStream_t);
 template cudaError_t launch_tile_init<float>(const float2*, const DictGeo*, const OwnGeo*, int, int64_t, int,

@@ -21,6 +21,10 @@ template <typename R>
 cudaError_t launch_tile_init(const typename cplx<R>::t* grid, const DictGeo* dg, const OwnGeo* own, int W,
                              int64_t total, int C, int64_t Lc, int TW, Rec<R>* rec, cudaStream_t st);
 
+template <typename R>
+cudaError_t launch_grid_export(const typename cplx<R>::t* grid, const DictGeo* dg, int W, int64_t P, double2* out,
+                               cudaStream_t st);
+
 // persistent MP loop (mploop.cu)
 struct AtomOut {  // identical layout to mpg_atom
   int32_t w, m, n, flags;

@@ -91,6 +91,7 @@ struct mpgabor {
   DevBuf prof;
   cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   float t_dgt = 0, t_init = 0, t_loop = 0;
+  int64_t launches = 0;  // kernels of this library enqueued through this handle
 
   int fail(int code, const std::string& msg) {
     err = msg;
@@ -109,6 +110,13 @@ struct mpgabor {
   do {                                                   \
     cudaError_t e__ = (expr);                            \
     if (e__ != cudaSuccess) return (h)->cuda_fail(e__, #expr); \
+  } while (0)
+
+// a launcher call that enqueues n of this library's kernels (counted for the bench)
+#define TRY_LAUNCH(h, n, expr) \
+  do {                         \
+    TRY_CUDA(h, expr);         \
+    (h)->launches += (n);      \
   } while (0)
 
 static int enter_device(mpgabor* h) {
@@ -218,13 +226,13 @@ extern "C" int mpgabor_kernels(mpgabor* h, double thr, void* stream) {
   // tables
   TRY_CUDA(h, h->tw.ensure(sizeof(double2) * (h->twres / 2 + 1)));
   TRY_CUDA(h, h->roots.ensure(sizeof(double2) * h->Rmax));
-  TRY_CUDA(h, launch_tables(h->tw.as<double2>(), h->twres, h->roots.as<double2>(), h->Rmax, st));
+  TRY_LAUNCH(h, 1, launch_tables(h->tw.as<double2>(), h->twres, h->roots.as<double2>(), h->Rmax, st));
   h->win_off.assign(W + 1, 0);
   for (int w = 0; w < W; ++w) h->win_off[w + 1] = h->win_off[w] + h->dicts[w].gl;
   TRY_CUDA(h, h->win.ensure(sizeof(double) * h->win_off[W]));
   for (int w = 0; w < W; ++w) {
     const mpg_dict& d = h->dicts[w];
-    TRY_CUDA(h, launch_window(d.win, d.gl, d.a, d.M, h->win.as<double>() + h->win_off[w], st));
+    TRY_LAUNCH(h, 1, launch_window(d.win, d.gl, d.a, d.M, h->win.as<double>() + h->win_off[w], st));
   }
   // pass 1: per pair lag range, max, box
   h->pairs.assign(W * W, PairGeo{});
@@ -265,10 +273,10 @@ extern "C" int mpgabor_kernels(mpgabor* h, double thr, void* stream) {
       const mpg_dict &du = h->dicts[u], &dv = h->dicts[v];
       PairGeo& pg = h->pairs[i];
       unsigned char* base = h->mxbox.as<unsigned char>() + 64 * i;
-      TRY_CUDA(h, launch_kern_rows(pg.a_c, pg.M_c, h->nu_first[i], h->nlag[i], h->win.as<double>() + h->win_off[u],
+      TRY_LAUNCH(h, 1, launch_kern_rows(pg.a_c, pg.M_c, h->nu_first[i], h->nlag[i], h->win.as<double>() + h->win_off[u],
                                    du.gl, h->win.as<double>() + h->win_off[v], dv.gl, h->tw.as<double2>(), h->twres,
                                    h->Hscratch.as<double2>(), st));
-      TRY_CUDA(h, launch_kern_max_box(h->Hscratch.as<double2>(), h->nlag[i], pg.M_c, h->nu_first[i], thr,
+      TRY_LAUNCH(h, 2, launch_kern_max_box(h->Hscratch.as<double2>(), h->nlag[i], pg.M_c, h->nu_first[i], thr,
                                       reinterpret_cast<unsigned long long*>(base), reinterpret_cast<int*>(base + 8),
                                       st));
     }
@@ -323,17 +331,17 @@ extern "C" int mpgabor_kernels(mpgabor* h, double thr, void* stream) {
       const mpg_dict &du = h->dicts[u], &dv = h->dicts[v];
       const PairGeo& pg = h->pairs[i];
       unsigned char* base = h->mxbox.as<unsigned char>() + 64 * i;
-      TRY_CUDA(h, launch_kern_rows(pg.a_c, pg.M_c, h->nu_first[i], h->nlag[i], h->win.as<double>() + h->win_off[u],
+      TRY_LAUNCH(h, 1, launch_kern_rows(pg.a_c, pg.M_c, h->nu_first[i], h->nlag[i], h->win.as<double>() + h->win_off[u],
                                    du.gl, h->win.as<double>() + h->win_off[v], dv.gl, h->tw.as<double2>(), h->twres,
                                    h->Hscratch.as<double2>(), st));
       RhoEnt* rrow = (u == v && h->rho_n[u] > 0) ? h->rho.as<RhoEnt>() + h->rho_off[u] : nullptr;
       if (h->f64())
-        TRY_CUDA(h, launch_kern_compact<double>(h->Hscratch.as<double2>(), pg.M_c, h->nu_first[i], thr,
+        TRY_LAUNCH(h, 1, launch_kern_compact<double>(h->Hscratch.as<double2>(), pg.M_c, h->nu_first[i], thr,
                                                 reinterpret_cast<const unsigned long long*>(base), pg,
                                                 h->kern.as<double2>(), h->boxcopy.as<double2>() + h->box_off[i],
                                                 rrow, st));
       else
-        TRY_CUDA(h, launch_kern_compact<float>(h->Hscratch.as<double2>(), pg.M_c, h->nu_first[i], thr,
+        TRY_LAUNCH(h, 1, launch_kern_compact<float>(h->Hscratch.as<double2>(), pg.M_c, h->nu_first[i], thr,
                                                reinterpret_cast<const unsigned long long*>(base), pg,
                                                h->kern.as<float2>(), h->boxcopy.as<double2>() + h->box_off[i], rrow,
                                                st));
@@ -610,25 +618,25 @@ extern "C" int mpgabor_run(mpgabor* h, const double* x_dev, int64_t Ls, int64_t 
   const int W = h->W;
   TRY_CUDA(h, cudaEventRecord(h->ev[0], st));
   TRY_CUDA(h, cudaMemsetAsync(h->flag.p, 0, sizeof(int), st));
-  TRY_CUDA(h, launch_pad_energy(x_dev, Ls, h->xp.as<double>(), h->L, h->partial.as<double>(), h->flag.as<int>(),
+  TRY_LAUNCH(h, 2, launch_pad_energy(x_dev, Ls, h->xp.as<double>(), h->L, h->partial.as<double>(), h->flag.as<int>(),
                                 h->E0.as<double>(), st));
   for (int w = 0; w < W; ++w) {
     const DictGeo& d = h->geo[w];
     const double* g = h->win.as<double>() + h->win_off[w];
     if (h->f64())
-      TRY_CUDA(h, launch_dgt<double>(h->xp.as<double>(), h->L, d, g, h->tw.as<double2>(), h->twres,
+      TRY_LAUNCH(h, 1, launch_dgt<double>(h->xp.as<double>(), h->L, d, g, h->tw.as<double2>(), h->twres,
                                      h->grid.as<double2>() + d.grid_off, st));
     else
-      TRY_CUDA(h, launch_dgt<float>(h->xp.as<double>(), h->L, d, g, h->tw.as<double2>(), h->twres,
+      TRY_LAUNCH(h, 1, launch_dgt<float>(h->xp.as<double>(), h->L, d, g, h->tw.as<double2>(), h->twres,
                                     h->grid.as<float2>() + d.grid_off, st));
   }
   TRY_CUDA(h, cudaEventRecord(h->ev[1], st));
   LoopParams& P = h->lp;
   if (h->f64())
-    TRY_CUDA(h, launch_tile_init<double>(h->grid.as<double2>(), h->d_geo.as<DictGeo>(), h->d_own.as<OwnGeo>(), W, h->total_tiles, P.C, P.Lc,
+    TRY_LAUNCH(h, 2, launch_tile_init<double>(h->grid.as<double2>(), h->d_geo.as<DictGeo>(), h->d_own.as<OwnGeo>(), W, h->total_tiles, P.C, P.Lc,
                                          h->TW, h->rec.as<Rec<double>>(), st));
   else
-    TRY_CUDA(h, launch_tile_init<float>(h->grid.as<float2>(), h->d_geo.as<DictGeo>(), h->d_own.as<OwnGeo>(), W, h->total_tiles, P.C, P.Lc,
+    TRY_LAUNCH(h, 2, launch_tile_init<float>(h->grid.as<float2>(), h->d_geo.as<DictGeo>(), h->d_own.as<OwnGeo>(), W, h->total_tiles, P.C, P.Lc,
                                         h->TW, h->rec.as<Rec<float>>(), st));
   if (coef_dev) TRY_CUDA(h, cudaMemsetAsync(coef_dev, 0, sizeof(double2) * h->P_R, st));
   TRY_CUDA(h, cudaMemcpyAsync(energy_dev, h->E0.p, sizeof(double), cudaMemcpyDeviceToDevice, st));
@@ -667,7 +675,7 @@ extern "C" int mpgabor_run(mpgabor* h, const double* x_dev, int64_t Ls, int64_t 
     P.prof = h->prof.as<long long>();
   }
   TRY_CUDA(h, cudaEventRecord(h->ev[3], st));
-  TRY_CUDA(h, launch_mp_loop(P, h->f64(), h->threads, st));
+  TRY_LAUNCH(h, 1, launch_mp_loop(P, h->f64(), h->threads, st));
   TRY_CUDA(h, cudaEventRecord(h->ev[4], st));
   LoopResult lr{};
   TRY_CUDA(h, cudaMemcpyAsync(&lr, h->result.p, sizeof lr, cudaMemcpyDeviceToHost, st));
@@ -685,6 +693,22 @@ extern "C" int mpgabor_run(mpgabor* h, const double* x_dev, int64_t Ls, int64_t 
   return MPG_OK;
 }
 
+extern "C" int mpgabor_residual(mpgabor* h, double* out_dev, void* stream) {
+  if (!h || !out_dev) return MPG_EINVAL;
+  if (h->L < 0 || !h->have_kernels) return h->fail(MPG_ESTATE, "no run yet");
+  int rc = enter_device(h);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (h->f64())
+    TRY_LAUNCH(h, 1, launch_grid_export<double>(h->grid.as<double2>(), h->d_geo.as<DictGeo>(), h->W, h->P_R,
+                                           reinterpret_cast<double2*>(out_dev), st));
+  else
+    TRY_LAUNCH(h, 1, launch_grid_export<float>(h->grid.as<float2>(), h->d_geo.as<DictGeo>(), h->W, h->P_R,
+                                          reinterpret_cast<double2*>(out_dev), st));
+  TRY_CUDA(h, cudaStreamSynchronize(st));
+  return MPG_OK;
+}
+
 extern "C" int mpgabor_set_profile(mpgabor* h, int32_t mode) {
   if (!h) return MPG_EINVAL;
   if (mode < 0 || mode > 3) return h->fail(MPG_EINVAL, "profile mode must be in [0, 3]");
@@ -695,6 +719,12 @@ extern "C" int mpgabor_set_profile(mpgabor* h, int32_t mode) {
 extern "C" int mpgabor_last_profile(const mpgabor* h, int64_t* cycles) {
   if (!h || !cycles) return MPG_EINVAL;
   for (int i = 0; i < 8; ++i) cycles[i] = h->prof_host[i];
+  return MPG_OK;
+}
+
+extern "C" int mpgabor_launch_count(const mpgabor* h, int64_t* n) {
+  if (!h || !n) return MPG_EINVAL;
+  *n = h->launches;
   return MPG_OK;
 }
 
@@ -725,12 +755,12 @@ extern "C" int mpgabor_synth(mpgabor* h, const mpg_atom* atoms_dev, int64_t n_at
   for (auto& d : h->geo) fmax = std::max(fmax, (int64_t)d.N * d.M);
   TRY_CUDA(h, h->frames.ensure(sizeof(double) * fmax));
   TRY_CUDA(h, cudaMemsetAsync(h->sol.p, 0, sizeof(double2) * h->P_R, st));
-  TRY_CUDA(h, launch_synth_scatter(reinterpret_cast<const AtomOut*>(atoms_dev), n_atoms, h->d_geo.as<DictGeo>(), h->W,
+  TRY_LAUNCH(h, (n_atoms > 0 ? 1 : 0), launch_synth_scatter(reinterpret_cast<const AtomOut*>(atoms_dev), n_atoms, h->d_geo.as<DictGeo>(), h->W,
                                    h->sol.as<double2>(), st));
   for (int w = 0; w < h->W; ++w) {
     const DictGeo& d = h->geo[w];
-    TRY_CUDA(h, launch_synth_frames(h->sol.as<double2>(), d, h->tw.as<double2>(), h->twres, h->frames.as<double>(), st));
-    TRY_CUDA(h, launch_synth_ola(h->frames.as<double>(), d, h->win.as<double>() + h->win_off[w], Ls, y_dev, w > 0, st));
+    TRY_LAUNCH(h, 1, launch_synth_frames(h->sol.as<double2>(), d, h->tw.as<double2>(), h->twres, h->frames.as<double>(), st));
+    TRY_LAUNCH(h, 1, launch_synth_ola(h->frames.as<double>(), d, h->win.as<double>() + h->win_off[w], Ls, y_dev, w > 0, st));
   }
   return MPG_OK;
 }

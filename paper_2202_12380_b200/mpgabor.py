@@ -71,6 +71,8 @@ _SIGS = {
                            ctypes.c_int),
     "mpgabor_last_timing": ([_P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
                              ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
+    "mpgabor_residual": ([_P, _P, _P], ctypes.c_int),
+    "mpgabor_launch_count": ([_P, ctypes.POINTER(_I64)], ctypes.c_int),
     "mpgabor_set_profile": ([_P, _I32], ctypes.c_int),
     "mpgabor_last_profile": ([_P, ctypes.POINTER(_I64)], ctypes.c_int),
     "mpgabor_destroy": ([_P], None),
@@ -197,6 +199,16 @@ def mpgabor_last_timing(h):
     return a.value, b.value, c.value
 
 
+def mpgabor_residual(h, out_dev, stream=None):
+    _check(h, _lib.mpgabor_residual(h, _ptr(out_dev), _stream(stream)))
+
+
+def mpgabor_launch_count(h):
+    n = _I64()
+    _check(h, _lib.mpgabor_launch_count(h, ctypes.byref(n)))
+    return n.value
+
+
 def mpgabor_set_profile(h, mode):
     _check(h, _lib.mpgabor_set_profile(h, int(mode)))
 
@@ -313,6 +325,17 @@ class MPGabor:
 
     def kernel_box(self, u, v):
         return mpgabor_kernel_box(self.h, u, v)
+
+    def residual(self, Ls, stream=None):
+        """Residual c^ of the last run as a complex128 torch tensor [P_R] on the device."""
+        torch = self.torch
+        P = self.layout(Ls)[3][-1]
+        out = torch.empty(2 * P, dtype=torch.float64, device="cuda")
+        mpgabor_residual(self.h, out, stream)
+        return out.view(torch.complex128)
+
+    def launch_count(self):
+        return mpgabor_launch_count(self.h)
 
     def set_profile(self, mode):
         mpgabor_set_profile(self.h, mode)

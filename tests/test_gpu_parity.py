@@ -1,0 +1,339 @@
+"""GPU parity: the CUDA path through the C ABI against the oracle (B200 only).
+
+Acceptance (BASELINE.json north_star):
+  fp64: identical atom-index sequence and |E_k^gpu - E_k^or| / E_k^or <= 1e-9 at every k;
+  fp32: identical indices up to the first near-tie (oracle gap < 1e-6), final energy
+        estimate within 1e-4 of E_0 (reading Z20).
+Full-size configs that the oracle cannot finish in seconds are checked on a prefix
+of the same run plus, at full length, sampled residual coefficients recomputed one
+by one by the oracle (gabor.residual_at) and the E_k recurrence recomputed from the
+atom list.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import siggen
+from siggen import Dict, HANN, BLACKMAN, GAUSS, CONFIGS, random_signal
+import oracle
+from oracle import gabor, loop as oloop, dense
+
+pytestmark = pytest.mark.gpu
+
+FP64_E_TOL = 1e-9
+NEAR_TIE = 1e-6
+
+
+@pytest.fixture(scope="module")
+def mpg():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2202_12380_b200.build import build_library
+    build_library()
+    import paper_2202_12380_b200.mpgabor as m
+    return m
+
+
+_SETUPS = {}
+_REFS = {}
+
+
+def setup_of(name):
+    if name not in _SETUPS:
+        cfg = CONFIGS[name]
+        x = siggen.signal(cfg)
+        _SETUPS[name] = (x, oracle.Setup.build(x, cfg.dicts, cfg.thr))
+    return _SETUPS[name]
+
+
+def ref_of(name, K):
+    key = (name, K)
+    if key not in _REFS:
+        cfg = CONFIGS[name]
+        x, S = setup_of(name)
+        _REFS[key] = oloop.mp_run(S, K, cfg.errdb)
+    return _REFS[key]
+
+
+def gpu_run(mpg, dicts, thr, x, K, errdb, prec="f64", launch=None, want_coef=False):
+    mp = mpg.MPGabor(dicts, thr, prec)
+    if launch:
+        mp.set_launch(*launch)
+    out = mp.run(torch.from_numpy(np.ascontiguousarray(x)).cuda(), K, errdb, want_coef=want_coef)
+    lay = mp.layout(x.size)
+    return mp, out, out.index(lay[3], lay[2])
+
+
+def first_divergence(a, b):
+    n = min(a.size, b.size)
+    d = np.nonzero(a[:n] != b[:n])[0]
+    return int(d[0]) if d.size else (n if a.size == b.size else n)
+
+
+def assert_fp64_parity(out, idx, ref):
+    assert out.n == ref.n and out.stop == ref.stop, (out.n, ref.n, out.stop_name, ref.stop_name)
+    assert np.array_equal(idx, ref.index), f"first divergence at {first_divergence(idx, ref.index)}"
+    rel = np.abs(out.energy - ref.energy) / np.abs(ref.energy)
+    assert rel.max() <= FP64_E_TOL, rel.max()
+
+
+def assert_fp32_parity(out, idx, ref, E0):
+    d = first_divergence(idx, ref.index)
+    if d < min(out.n, ref.n):
+        # divergence is only allowed at or after a near-tie of the oracle
+        assert ref.gaps[: d + 1].min() < NEAR_TIE, (d, ref.gaps[: d + 1].min())
+    assert abs(out.energy[-1] - ref.energy[-1]) / E0 <= 1e-4
+
+
+# ---------------------------------------------------------------------------
+# kernels (N2) and DGT (N1)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("name", ["C0", "C1", "C2", "C3", "C4"])
+def test_kernels_match_oracle(mpg, name):
+    cfg = CONFIGS[name]
+    x, S = setup_of(name)
+    mp = mpg.MPGabor(cfg.dicts, cfg.thr, "f64")
+    W = len(cfg.dicts)
+    box_total, kept, _ = mp.kernel_stats()
+    assert box_total == sum(k.h.size for k in S.K)
+    assert kept == sum(k.kept for k in S.K)
+    for u in range(W):
+        for v in range(W):
+            K = S.K[u * W + v]
+            box, vals, mx = mp.kernel_box(u, v)
+            assert box == (K.mu_lo, K.mu_hi, K.nu_lo, K.nu_hi), (u, v)
+            assert np.array_equal(vals != 0, K.h != 0), (u, v)    # identical kept-entry sets
+            assert np.max(np.abs(vals - K.h)) <= 1e-13 * K.mx, (u, v)
+            assert abs(mx - K.mx) <= 1e-13 * K.mx
+    mp.close()
+
+
+@pytest.mark.parametrize("name,prec", [("C0", "f64"), ("C2", "f64"), ("C3", "f64"), ("C2", "f32"),
+                                       ("C4", "f64")])
+def test_dgt_matches_oracle(mpg, name, prec):
+    cfg = CONFIGS[name]
+    x, S = setup_of(name)
+    mp, out, _ = gpu_run(mpg, cfg.dicts, cfg.thr, x, 0, cfg.errdb, prec)
+    res = mp.residual(cfg.Ls).cpu().numpy()
+    ref = np.concatenate([g.ravel() for g in S.grids])
+    scale = math.sqrt(S.E0)
+    tol = 1e-12 if prec == "f64" else 1e-6
+    assert np.max(np.abs(res - ref)) <= tol * scale
+    assert out.n == 0 and abs(out.E0 - S.E0) <= 1e-12 * S.E0
+    mp.close()
+
+
+# ---------------------------------------------------------------------------
+# full runs
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("name", ["C0", "C1", "C2"])
+def test_full_run_fp64(mpg, name):
+    cfg = CONFIGS[name]
+    x, S = setup_of(name)
+    ref = ref_of(name, cfg.maxit)
+    mp, out, idx = gpu_run(mpg, cfg.dicts, cfg.thr, x, cfg.maxit, cfg.errdb, "f64", want_coef=True)
+    assert_fp64_parity(out, idx, ref)
+    np.testing.assert_allclose(out.atoms["re"], ref.atoms["re"], rtol=0, atol=1e-9 * math.sqrt(S.E0))
+    np.testing.assert_allclose(out.atoms["im"], ref.atoms["im"], rtol=0, atol=1e-9 * math.sqrt(S.E0))
+    assert np.array_equal(out.atoms["flags"], ref.atoms["flags"])
+    # final residual and solution vectors
+    res = mp.residual(cfg.Ls).cpu().numpy()
+    assert np.max(np.abs(res - ref.res)) <= 1e-9 * math.sqrt(S.E0)
+    coef = out.coef.cpu().numpy()
+    assert np.max(np.abs(coef - ref.sol)) <= 1e-9 * math.sqrt(S.E0)
+    # synthesis (N6) against the oracle's Eq. (18)
+    y = mp.synth(out.atoms_dev, out.n, cfg.Ls).cpu().numpy()
+    yref = gabor.synthesize(ref.atoms, cfg.dicts, S.lay.L, cfg.Ls)
+    assert np.max(np.abs(y - yref)) <= 1e-11 * np.max(np.abs(yref))
+    mp.close()
+
+
+@pytest.mark.parametrize("name", ["C0", "C1", "C2"])
+def test_full_run_fp32(mpg, name):
+    cfg = CONFIGS[name]
+    x, S = setup_of(name)
+    ref = ref_of(name, cfg.maxit)
+    mp, out, idx = gpu_run(mpg, cfg.dicts, cfg.thr, x, cfg.maxit, cfg.errdb, "f32")
+    assert_fp32_parity(out, idx, ref, S.E0)
+    mp.close()
+
+
+PREFIX = {"C3": 20000, "C4": 4000}
+
+
+@pytest.mark.parametrize("name,prec", [("C3", "f64"), ("C4", "f64"), ("C3", "f32"), ("C4", "f32")])
+def test_prefix_parity_large(mpg, name, prec):
+    cfg = CONFIGS[name]
+    x, S = setup_of(name)
+    K = PREFIX[name]
+    ref = ref_of(name, K)
+    mp, out, idx = gpu_run(mpg, cfg.dicts, cfg.thr, x, K, cfg.errdb, prec)
+    if prec == "f64":
+        assert_fp64_parity(out, idx, ref)
+    else:
+        assert_fp32_parity(out, idx, ref, S.E0)
+    mp.close()
+
+
+def _energy_recurrence(setup, atoms, E0):
+    """E_k recomputed from the atom list with the oracle's kernels (Eq. (20), rho from h_uu)."""
+    W = len(setup.dicts)
+    X, Y = atoms["re"], atoms["im"]
+    rho = np.zeros(atoms.size, dtype=np.complex128)
+    for u in range(W):
+        sel = np.nonzero(atoms["w"] == u)[0]
+        K = setup.K[u * W + u]
+        M = setup.dicts[u].M
+        mu = (-2 * atoms["m"][sel].astype(np.int64)) % M
+        mu = np.where(2 * mu > M, mu - M, mu)
+        ok = (mu >= K.mu_lo) & (mu <= K.mu_hi) & (K.nu_lo <= 0) & (K.nu_hi >= 0)
+        rho[sel[ok]] = K.h[-K.nu_lo, mu[ok] - K.mu_lo]
+    Et = 2 * (X * X + Y * Y + rho.real * (X * X - Y * Y) - 2 * rho.imag * X * Y)
+    Et = np.where(atoms["flags"] & 1, X * X, Et)
+    return E0 - np.concatenate([[0.0], np.cumsum(Et)])
+
+
+@pytest.mark.parametrize("name,prec", [("C3", "f64"), ("C4", "f64"), ("C4", "f32")])
+def test_full_length_sampled(mpg, name, prec):
+    """BASELINE sizes in the bench launch configuration: sampled residual coefficients
+    recomputed one by one by the oracle from the GPU's own atom list, and the E_k trace
+    re-derived from that list."""
+    cfg = CONFIGS[name]
+    x, S = setup_of(name)
+    mp, out, idx = gpu_run(mpg, cfg.dicts, cfg.thr, x, cfg.maxit, cfg.errdb, prec)
+    # K = maxit, or earlier by the E_k < 0 heuristic that C3 reaches near 1.05e5
+    assert out.n > 50_000 and out.stop_name in ("maxit", "negest"), (out.n, out.stop_name)
+    assert np.all(np.diff(out.energy) <= 0)
+    Erec = _energy_recurrence(S, out.atoms, out.E0)
+    assert np.max(np.abs(Erec - out.energy)) <= 1e-9 * out.E0
+    res = mp.residual(cfg.Ls).cpu().numpy()
+    rng = np.random.default_rng(7)
+    last = idx[-30:]
+    pts = np.unique(np.clip(np.concatenate([last, last + 1, last - 1, rng.integers(0, S.lay.P, 30)]),
+                            0, S.lay.P - 1))
+    want = gabor.residual_at(S, out.atoms, pts)
+    tol = 1e-9 if prec == "f64" else 2e-3
+    assert np.max(np.abs(res[pts] - want)) <= tol * math.sqrt(S.E0)
+    mp.close()
+
+
+# ---------------------------------------------------------------------------
+# launch configurations, determinism, host API
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("launch", [(1, 512, 64, 0), (2, 128, 32, 1), (4, 256, 128, 1), (8, 512, 64, 2),
+                                    (16, 256, 32, 2), (16, 512, 128, 1)])
+def test_launch_configurations_identical(mpg, launch):
+    cfg = CONFIGS["C1"]
+    x, S = setup_of("C1")
+    ref = ref_of("C1", 3000)
+    mp, out, idx = gpu_run(mpg, cfg.dicts, cfg.thr, x, 3000, cfg.errdb, "f64", launch=launch)
+    info = mp.launch_info()
+    assert info["cluster"] == launch[0] and info["tile_width"] == launch[2]
+    assert_fp64_parity(out, idx, ref)
+    mp.close()
+
+
+def test_deterministic(mpg):
+    cfg = CONFIGS["C2"]
+    x, _ = setup_of("C2")
+    mp = mpg.MPGabor(cfg.dicts, cfg.thr, "f64")
+    xd = torch.from_numpy(x).cuda()
+    a = mp.run(xd, 5000, cfg.errdb)
+    b = mp.run(xd, 5000, cfg.errdb)
+    assert a.atoms.tobytes() == b.atoms.tobytes() and a.energy.tobytes() == b.energy.tobytes()
+    mp.close()
+
+
+def test_decompose_host_matches_device(mpg):
+    cfg = CONFIGS["C1"]
+    x, S = setup_of("C1")
+    h = mpg.mpgabor_create(cfg.dicts, mpg.MPG_F64)
+    mpg.mpgabor_kernels(h, cfg.thr)
+    K = 2000
+    atoms = np.zeros(K, dtype=mpg.ATOM_DTYPE)
+    energy = np.zeros(K + 1)
+    y = np.zeros(cfg.Ls)
+    res = mpg.mpgabor_decompose_host(h, np.ascontiguousarray(x), K, cfg.errdb, atoms, energy, y)
+    mpg.mpgabor_destroy(h)
+    ref = ref_of("C1", K)
+    assert res.n_atoms == K
+    off, MR = np.asarray(S.lay.off), np.asarray(S.lay.MR)
+    idx = off[atoms["w"]] + atoms["n"].astype(np.int64) * MR[atoms["w"]] + atoms["m"]
+    assert np.array_equal(idx, ref.index)
+    yref = gabor.synthesize(ref.atoms, cfg.dicts, S.lay.L, cfg.Ls)
+    assert np.max(np.abs(y - yref)) <= 1e-11 * np.max(np.abs(yref))
+
+
+# ---------------------------------------------------------------------------
+# edge cases
+# ---------------------------------------------------------------------------
+def test_zero_signal_and_maxit_zero(mpg):
+    d = (Dict(HANN, 64, 16, 64),)
+    mp, out, _ = gpu_run(mpg, d, 1e-4, np.zeros(1024), 100, -math.inf)
+    assert out.n == 0 and out.stop_name == "zero"
+    mp.close()
+    mp, out, _ = gpu_run(mpg, d, 1e-4, np.zeros(1024), 100, -40.0)
+    assert out.n == 0 and out.stop_name == "errtol"
+    mp.close()
+    mp, out, _ = gpu_run(mpg, d, 1e-4, random_signal(1024, 1), 0, -math.inf)
+    assert out.n == 0 and out.stop_name == "maxit"
+    mp.close()
+
+
+def test_nonfinite_rejected(mpg):
+    x = random_signal(1024, 2)
+    x[100] = np.nan
+    mp = mpg.MPGabor((Dict(HANN, 64, 16, 64),), 1e-4, "f64")
+    with pytest.raises(mpg.MpgError) as e:
+        mp.run(torch.from_numpy(x).cuda(), 10, -math.inf)
+    assert "ENONFINITE" in str(e.value)
+    mp.close()
+
+
+def test_too_short_signal_rejected(mpg):
+    mp = mpg.MPGabor((Dict(HANN, 256, 64, 256),), 1e-4, "f64")
+    with pytest.raises(mpg.MpgError) as e:
+        mp.run(torch.from_numpy(random_signal(200, 2)).cuda(), 10, -math.inf)
+    assert "ELEN" in str(e.value)
+    mp.close()
+
+
+TINY = [
+    ((Dict(HANN, 16, 4, 16), Dict(HANN, 8, 2, 8)), 96),
+    ((Dict(BLACKMAN, 32, 8, 32), Dict(HANN, 16, 4, 16), Dict(BLACKMAN, 8, 2, 16)), 200),   # ragged Ls
+    ((Dict(GAUSS, 41, 4, 16), Dict(HANN, 32, 8, 32)), 256),                                  # gl > M
+]
+
+
+@pytest.mark.parametrize("dicts,Ls", TINY)
+@pytest.mark.parametrize("thr", [0.0, 1e-4, 1e-2])
+def test_tiny_dictionaries(mpg, dicts, Ls, thr):
+    # stop at -60 dB so that E_k stays far from 0 (its relative error is ill-conditioned there)
+    x = random_signal(Ls, 11)
+    S = oracle.Setup.build(x, dicts, thr)
+    ref = oloop.mp_run(S, 150, -60.0)
+    mp, out, idx = gpu_run(mpg, dicts, thr, x, 150, -60.0, "f64")
+    assert_fp64_parity(out, idx, ref)
+    if thr == 0.0:   # eps = 0: equals exact signal-domain MP (Eq. (8))
+        at, e, te, _, _ = dense.signal_mp(x, dicts, 150, -60.0)
+        off, MR = np.asarray(S.lay.off), np.asarray(S.lay.MR)
+        sidx = off[at["w"]] + at["n"].astype(np.int64) * MR[at["w"]] + at["m"]
+        assert np.array_equal(idx, sidx)
+    mp.close()
+
+
+def test_planted_atoms_recovered_c0(mpg):
+    # C0: the 20 planted unit atoms dominate; the first selections find planted (m, n)
+    cfg = CONFIGS["C0"]
+    x, _ = setup_of("C0")
+    mp, out, _ = gpu_run(mpg, cfg.dicts, cfg.thr, x, 60, cfg.errdb)
+    rng = np.random.Generator(np.random.PCG64(cfg.seed))
+    planted = set()
+    for _ in range(20):
+        n = int(rng.integers(0, 64)); m = int(rng.integers(1, 128))
+        rng.uniform(0, 2 * np.pi); rng.uniform(0.1, 1.0)
+        planted.add((m, n))
+    found = {(int(a["m"]), int(a["n"])) for a in out.atoms[:40]}
+    assert len(planted & found) >= 18
+    mp.close()

@@ -150,3 +150,17 @@ def test_c0_recovers_planted_atoms_and_estimate_tracks_truth():
     est_db = 10 * np.log10(r.energy[-1] / S.E0)
     assert abs(true_db - est_db) < 1.0
     assert np.all(np.diff(r.energy) <= 0)
+
+
+def test_residual_at_one_by_one_equals_loop():
+    # the single-coefficient restatement of Alg. 3 (gabor.residual_at) reproduces the
+    # loop's residual; it is what the GPU tests use for sampled full-size checks
+    cfg = CONFIGS["C1"]
+    x = signal(cfg)
+    S = oracle.Setup.build(x, cfg.dicts, cfg.thr)
+    r = loop.mp_run(S, 2000)
+    rng = np.random.default_rng(3)
+    pts = np.unique(np.clip(np.concatenate([r.index[-40:], r.index[-40:] + 1, r.index[-40:] - 2,
+                                            rng.integers(0, S.lay.P, 40)]), 0, S.lay.P - 1))
+    got = gabor.residual_at(S, r.atoms, pts)
+    assert np.max(np.abs(got - r.res[pts])) < 1e-14 * math.sqrt(S.E0)
