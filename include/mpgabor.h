@@ -199,6 +199,15 @@ int mpgabor_set_profile(mpgabor* h, int32_t mode);
  * barrier, [6] upper levels + root publication; [7] iterations. */
 int mpgabor_last_profile(const mpgabor* h, int64_t* cycles);
 
+/* Event timeline of iterations [it0, it0+n) of the next runs (n = 0 disables):
+ * per iteration and CTA, `slots` int64 values (globaltimer ns unless noted):
+ * [0] roots received, [1] selection + scalar done, [2] geometry done, [3] after
+ * the block barrier, [4] root published, [5] items of the CTA (count), [6] dirty
+ * level-1 nodes (count), [7] clean-part max done, [8 + w] warp w finished its items. */
+int mpgabor_set_trace(mpgabor* h, int64_t it0, int32_t n);
+/* Copy the timeline (host int64[n * ctas * slots], row-major [it][cta][slot]). */
+int mpgabor_last_trace(mpgabor* h, int64_t* host, int64_t cap, int32_t* slots, int32_t* ctas);
+
 void mpgabor_destroy(mpgabor* h);
 
 /* Reason for the last failure on h (or of the last failed mpgabor_create when

@@ -72,6 +72,8 @@ struct mpgabor {
   // launch tuning
   int cluster_req = 0, threads = 512, TW_req = 0, srec_req = 0;  // 0 = automatic
   int TW = 64, srec = 0;
+  int run_threads = 512;  // threads of the planned loop launch
+  int kind = 0;           // loop kernel: 0 mploop.cu, 1 mplean.cu
 
   // per-length layout
   int64_t L = -1, Ls_cached = -1;
@@ -87,6 +89,9 @@ struct mpgabor {
   DevBuf sol, frames, hx, hatoms, henergy, hy;
 
   int prof_mode = 0;
+  long long trace_it0 = 0;
+  int trace_n = 0;
+  DevBuf trace;
   long long prof_host[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   DevBuf prof;
   cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -191,7 +196,7 @@ extern "C" void mpgabor_destroy(mpgabor* h) {
     cudaSetDevice(h->device);
     for (DevBuf* b : {&h->tw, &h->roots, &h->win, &h->kern, &h->boxcopy, &h->d_pairs, &h->rho, &h->rho_meta,
                       &h->Hscratch, &h->mxbox, &h->d_geo, &h->grid, &h->rec, &h->xp, &h->partial, &h->flag,
-                      &h->E0, &h->result, &h->sol, &h->frames, &h->hx, &h->hatoms, &h->henergy, &h->hy, &h->prof, &h->d_own})
+                      &h->E0, &h->result, &h->sol, &h->frames, &h->hx, &h->hatoms, &h->henergy, &h->hy, &h->prof, &h->d_own, &h->trace})
       b->release();
     for (auto e : h->ev)
       if (e) cudaEventDestroy(e);
@@ -234,17 +239,18 @@ extern "C" int mpgabor_kernels(mpgabor* h, double thr, void* stream) {
     const mpg_dict& d = h->dicts[w];
     TRY_LAUNCH(h, 1, launch_window(d.win, d.gl, d.a, d.M, h->win.as<double>() + h->win_off[w], st));
   }
-  // pass 1: per pair lag range, max, box
+  // per pair: common grid, lag range, rows h(m >= 0, nu) into its own scratch slice
   h->pairs.assign(W * W, PairGeo{});
   h->nu_first.assign(W * W, 0);
   h->nlag.assign(W * W, 0);
   h->pair_mx.assign(W * W, 0.0);
   h->pair_kept.assign(W * W, 0);
-  size_t hmax = 0;
+  std::vector<int64_t> hoff(W * W + 1, 0);
   for (int u = 0; u < W; ++u)
     for (int v = 0; v < W; ++v) {
+      const int i = u * W + v;
       const mpg_dict &du = h->dicts[u], &dv = h->dicts[v];
-      PairGeo& pg = h->pairs[u * W + v];
+      PairGeo& pg = h->pairs[i];
       pg.a_c = std::min(du.a, dv.a);
       pg.M_c = std::max(du.M, dv.M);
       pg.R = pg.M_c / pg.a_c;
@@ -252,12 +258,11 @@ extern "C" int mpgabor_kernels(mpgabor* h, double thr, void* stream) {
       pg.s_n = std::max(1, dv.a / pg.a_c);
       pg.rstep = h->Rmax / pg.R;
       int lo, hi;
-      const int n = overlap_lags(du, dv, pg.a_c, lo, hi);
-      h->nu_first[u * W + v] = lo;
-      h->nlag[u * W + v] = n;
-      hmax = std::max(hmax, (size_t)n * (pg.M_c / 2 + 1));
+      h->nlag[i] = overlap_lags(du, dv, pg.a_c, lo, hi);
+      h->nu_first[i] = lo;
+      hoff[i + 1] = hoff[i] + (int64_t)h->nlag[i] * (pg.M_c / 2 + 1);
     }
-  TRY_CUDA(h, h->Hscratch.ensure(sizeof(double2) * hmax));
+  TRY_CUDA(h, h->Hscratch.ensure(sizeof(double2) * hoff[W * W]));
   TRY_CUDA(h, h->mxbox.ensure(64 * W * W));
   std::vector<unsigned char> mb(64 * W * W);
   for (int i = 0; i < W * W; ++i) {
@@ -271,17 +276,18 @@ extern "C" int mpgabor_kernels(mpgabor* h, double thr, void* stream) {
     for (int v = 0; v < W; ++v) {
       const int i = u * W + v;
       const mpg_dict &du = h->dicts[u], &dv = h->dicts[v];
-      PairGeo& pg = h->pairs[i];
+      const PairGeo& pg = h->pairs[i];
       unsigned char* base = h->mxbox.as<unsigned char>() + 64 * i;
+      double2* H = h->Hscratch.as<double2>() + hoff[i];
       TRY_LAUNCH(h, 1, launch_kern_rows(pg.a_c, pg.M_c, h->nu_first[i], h->nlag[i], h->win.as<double>() + h->win_off[u],
-                                   du.gl, h->win.as<double>() + h->win_off[v], dv.gl, h->tw.as<double2>(), h->twres,
-                                   h->Hscratch.as<double2>(), st));
-      TRY_LAUNCH(h, 2, launch_kern_max_box(h->Hscratch.as<double2>(), h->nlag[i], pg.M_c, h->nu_first[i], thr,
-                                      reinterpret_cast<unsigned long long*>(base), reinterpret_cast<int*>(base + 8),
-                                      st));
+                                        du.gl, h->win.as<double>() + h->win_off[v], dv.gl, h->tw.as<double2>(),
+                                        h->twres, H, st));
+      TRY_LAUNCH(h, 2, launch_kern_max_box(H, h->nlag[i], pg.M_c, h->nu_first[i], thr,
+                                           reinterpret_cast<unsigned long long*>(base), reinterpret_cast<int*>(base + 8),
+                                           st));
     }
   TRY_CUDA(h, cudaMemcpyAsync(mb.data(), h->mxbox.p, mb.size(), cudaMemcpyDeviceToHost, st));
-  TRY_CUDA(h, cudaStreamSynchronize(st));
+  TRY_CUDA(h, cudaStreamSynchronize(st));   // the boxes size the kernel storage
   h->kern_elems = 0;
   h->box_total = 0;
   h->kept_total = 0;
@@ -324,27 +330,24 @@ extern "C" int mpgabor_kernels(mpgabor* h, double thr, void* stream) {
   TRY_CUDA(h, h->kern.ensure(h->celem() * std::max<int64_t>(1, h->kern_elems)));
   TRY_CUDA(h, h->boxcopy.ensure(sizeof(double2) * std::max<int64_t>(1, h->box_total)));
   TRY_CUDA(h, h->rho.ensure(sizeof(RhoEnt) * std::max(1, h->rho_total)));
-  // pass 2: recompute rows and compact
+  // compact every box into the per-alignment-class layout
   for (int u = 0; u < W; ++u)
     for (int v = 0; v < W; ++v) {
       const int i = u * W + v;
-      const mpg_dict &du = h->dicts[u], &dv = h->dicts[v];
       const PairGeo& pg = h->pairs[i];
       unsigned char* base = h->mxbox.as<unsigned char>() + 64 * i;
-      TRY_LAUNCH(h, 1, launch_kern_rows(pg.a_c, pg.M_c, h->nu_first[i], h->nlag[i], h->win.as<double>() + h->win_off[u],
-                                   du.gl, h->win.as<double>() + h->win_off[v], dv.gl, h->tw.as<double2>(), h->twres,
-                                   h->Hscratch.as<double2>(), st));
+      const double2* H = h->Hscratch.as<double2>() + hoff[i];
       RhoEnt* rrow = (u == v && h->rho_n[u] > 0) ? h->rho.as<RhoEnt>() + h->rho_off[u] : nullptr;
       if (h->f64())
-        TRY_LAUNCH(h, 1, launch_kern_compact<double>(h->Hscratch.as<double2>(), pg.M_c, h->nu_first[i], thr,
-                                                reinterpret_cast<const unsigned long long*>(base), pg,
-                                                h->kern.as<double2>(), h->boxcopy.as<double2>() + h->box_off[i],
-                                                rrow, st));
+        TRY_LAUNCH(h, 1, launch_kern_compact<double>(H, pg.M_c, h->nu_first[i], thr,
+                                                     reinterpret_cast<const unsigned long long*>(base), pg,
+                                                     h->kern.as<double2>(), h->boxcopy.as<double2>() + h->box_off[i],
+                                                     rrow, st));
       else
-        TRY_LAUNCH(h, 1, launch_kern_compact<float>(h->Hscratch.as<double2>(), pg.M_c, h->nu_first[i], thr,
-                                               reinterpret_cast<const unsigned long long*>(base), pg,
-                                               h->kern.as<float2>(), h->boxcopy.as<double2>() + h->box_off[i], rrow,
-                                               st));
+        TRY_LAUNCH(h, 1, launch_kern_compact<float>(H, pg.M_c, h->nu_first[i], thr,
+                                                    reinterpret_cast<const unsigned long long*>(base), pg,
+                                                    h->kern.as<float2>(), h->boxcopy.as<double2>() + h->box_off[i],
+                                                    rrow, st));
     }
   TRY_CUDA(h, h->d_pairs.ensure(sizeof(PairGeo) * W * W));
   TRY_CUDA(h, cudaMemcpyAsync(h->d_pairs.p, h->pairs.data(), sizeof(PairGeo) * W * W, cudaMemcpyHostToDevice, st));
@@ -357,7 +360,6 @@ extern "C" int mpgabor_kernels(mpgabor* h, double thr, void* stream) {
   TRY_CUDA(h, h->rho_meta.ensure(sizeof(int) * 3 * W));
   TRY_CUDA(h, cudaMemcpyAsync(h->rho_meta.p, meta.data(), sizeof(int) * 3 * W, cudaMemcpyHostToDevice, st));
   TRY_CUDA(h, cudaStreamSynchronize(st));
-  h->Hscratch.release();
   h->have_kernels = true;
   h->L = -1;  // layout depends on kernel boxes (validation), recompute at next run
   return MPG_OK;
@@ -512,7 +514,11 @@ static size_t plan_loop(mpgabor* h, int TW, int srec, int C) {
     n = (n + 31) / 32;
   }
   P.nlev = nl;
-  P.smem_bytes = loop_smem_bytes(P, h->f64());
+  // loop kernel: 0 = mploop.cu (default), 1 = mplean.cu (profile-mode bit 2)
+  const int kind = (h->prof_mode & 4) ? 1 : 0;
+  h->kind = kind;
+  h->run_threads = h->threads;
+  P.smem_bytes = kind == 1 ? lean_smem_bytes(P, h->f64()) : loop_smem_bytes(P, h->f64());
   return P.smem_bytes;
 }
 
@@ -552,7 +558,8 @@ static int ensure_layout(mpgabor* h, int64_t Ls) {
         why = "shared memory " + std::to_string(smem) + " B";
         break;  // smaller clusters need more per-CTA memory
       }
-      const int cmax = loop_max_cluster(h->f64(), c.srec, c.TW, h->threads, smem);
+      const int cmax = h->kind == 1 ? lean_max_cluster(h->f64(), c.srec, c.TW, h->run_threads, smem)
+                                    : loop_max_cluster(h->f64(), c.srec, c.TW, h->run_threads, smem);
       if (cmax >= C) {
         ok = true;
         break;
@@ -591,7 +598,7 @@ extern "C" int mpgabor_launch_info(const mpgabor* h, int32_t* cluster, int32_t* 
   if (!h) return MPG_EINVAL;
   if (h->L < 0) return const_cast<mpgabor*>(h)->fail(MPG_ESTATE, "no run yet");
   if (cluster) *cluster = h->lp.C;
-  if (threads) *threads = h->threads;
+  if (threads) *threads = h->run_threads;
   if (tile_width) *tile_width = h->TW;
   if (records) *records = h->srec ? 1 : 2;
   if (smem_bytes) *smem_bytes = (int64_t)h->lp.smem_bytes;
@@ -668,6 +675,16 @@ extern "C" int mpgabor_run(mpgabor* h, const double* x_dev, int64_t Ls, int64_t 
   P.sol = reinterpret_cast<double2*>(coef_dev);
   P.result = h->result.as<LoopResult>();
   P.floor_mode = (h->prof_mode & 2) ? 1 : 0;
+  P.trace = nullptr;
+  P.trace_it0 = h->trace_it0;
+  P.trace_n = h->trace_n;
+  P.trace_slots = 13 + h->run_threads / 32;
+  if (h->trace_n > 0) {
+    const size_t tb = sizeof(long long) * (size_t)h->trace_n * P.C * P.trace_slots;
+    TRY_CUDA(h, h->trace.ensure(tb));
+    TRY_CUDA(h, cudaMemsetAsync(h->trace.p, 0, tb, st));
+    P.trace = h->trace.as<long long>();
+  }
   P.prof = nullptr;
   if (h->prof_mode & 1) {
     TRY_CUDA(h, h->prof.ensure(sizeof(long long) * 8));
@@ -675,7 +692,10 @@ extern "C" int mpgabor_run(mpgabor* h, const double* x_dev, int64_t Ls, int64_t 
     P.prof = h->prof.as<long long>();
   }
   TRY_CUDA(h, cudaEventRecord(h->ev[3], st));
-  TRY_LAUNCH(h, 1, launch_mp_loop(P, h->f64(), h->threads, st));
+  if (h->kind == 1)
+    TRY_LAUNCH(h, 1, launch_lean_loop(P, h->f64(), h->run_threads, st));
+  else
+    TRY_LAUNCH(h, 1, launch_mp_loop(P, h->f64(), h->run_threads, st));
   TRY_CUDA(h, cudaEventRecord(h->ev[4], st));
   LoopResult lr{};
   TRY_CUDA(h, cudaMemcpyAsync(&lr, h->result.p, sizeof lr, cudaMemcpyDeviceToHost, st));
@@ -709,9 +729,32 @@ extern "C" int mpgabor_residual(mpgabor* h, double* out_dev, void* stream) {
   return MPG_OK;
 }
 
+extern "C" int mpgabor_set_trace(mpgabor* h, int64_t it0, int32_t n) {
+  if (!h || it0 < 0 || n < 0) return MPG_EINVAL;
+  h->trace_it0 = it0;
+  h->trace_n = n;
+  return MPG_OK;
+}
+
+extern "C" int mpgabor_last_trace(mpgabor* h, int64_t* host, int64_t cap, int32_t* slots, int32_t* ctas) {
+  if (!h) return MPG_EINVAL;
+  const int S = 13 + h->run_threads / 32;
+  if (slots) *slots = S;
+  if (ctas) *ctas = h->lp.C;
+  const int64_t need = (int64_t)h->trace_n * h->lp.C * S;
+  if (host && need > 0) {
+    if (cap < need) return h->fail(MPG_EINVAL, "trace buffer too small");
+    int rc = enter_device(h);
+    if (rc) return rc;
+    TRY_CUDA(h, cudaMemcpy(host, h->trace.p, sizeof(int64_t) * need, cudaMemcpyDeviceToHost));
+  }
+  return MPG_OK;
+}
+
 extern "C" int mpgabor_set_profile(mpgabor* h, int32_t mode) {
   if (!h) return MPG_EINVAL;
-  if (mode < 0 || mode > 3) return h->fail(MPG_EINVAL, "profile mode must be in [0, 3]");
+  if (mode < 0 || mode > 7) return h->fail(MPG_EINVAL, "profile mode must be in [0, 7]");
+  if ((mode & 4) != (h->prof_mode & 4)) h->L = -1;  // bit 2 switches the loop kernel: re-plan
   h->prof_mode = mode;
   return MPG_OK;
 }
