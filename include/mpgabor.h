@@ -69,6 +69,8 @@ typedef struct {
   int32_t cluster;     /* CTAs in the thread-block cluster that ran the loop    */
   double E0;           /* ||x||^2                                                */
   double E_final;      /* energy estimate E_k after the last selection (Alg. 1)  */
+  int64_t rounds;      /* persistent-loop rounds (multi-selection: several atoms
+                          per round, see mpgabor_set_batch; otherwise n_atoms+1) */
 } mpg_result;
 
 enum { /* stop reasons, tested in this order before each selection (Z15) */
@@ -154,6 +156,15 @@ int mpgabor_decompose_host(mpgabor* h, const double* x_host, int64_t Ls, int64_t
  * tile width 64, else 128, else global records).  Takes effect at the next run. */
 int mpgabor_set_launch(mpgabor* h, int32_t cluster, int32_t threads, int32_t tile_width, int32_t records);
 
+/* Exact multi-selection: max_batch = the
+ * most atoms one loop round may select and update at once.  Every round's extra
+ * atoms are verified against the sequential argmax rule (Alg. 1, ties
+ * Z10) and rolled back bit-exactly when the proof fails, so the atom sequence,
+ * coefficients and energies are those of the one-selection loop for every value.
+ * 0 = automatic (the largest batch, 8), 1 = one selection per iteration (the
+ * plain persistent loop), 2..8 = that batch.  EINVAL outside [0, 8].  Takes
+ * effect at the next run. */
+int mpgabor_set_batch(mpgabor* h, int32_t max_batch);
 /* The launch plan used by the last mpgabor_run (host outputs, may be NULL);
  * records: 1 shared memory, 2 global memory. */
 int mpgabor_launch_info(const mpgabor* h, int32_t* cluster, int32_t* threads, int32_t* tile_width,

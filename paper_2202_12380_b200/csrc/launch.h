@@ -35,6 +35,7 @@ struct LoopResult {
   int stop;
   int pad;
   double E_final;
+  long long rounds;              // loop rounds (multi-selection kernel; = n_done + 1 for the others)
 };
 
 constexpr int MAX_LEVELS = 6;
@@ -72,6 +73,9 @@ struct LoopParams {
   long long* trace;              // optional event timeline (globaltimer ns), see mpgabor_set_trace
   long long trace_it0;
   int trace_n, trace_slots;
+  int spec;                      // multi-selection: candidates per round (1..multi_max_batch())
+  void* backup;                  // multi-selection: per-CTA tile backups [C][bk_cap][TW] (cplx<R>)
+  long long bk_cap;              // items per CTA per round the backup holds
   size_t smem_bytes;
 };
 
@@ -79,6 +83,14 @@ struct LoopParams {
 size_t loop_smem_bytes(const LoopParams& P, bool f64);
 cudaError_t launch_mp_loop(const LoopParams& P, bool f64, int threads, cudaStream_t st);
 int loop_max_cluster(bool f64, bool srec, int TW, int threads, size_t smem);
+
+// exact multi-selection loop kernel (mpmulti.cu, the default): MULTI_K = length of
+// every CTA's published top-K tile list
+constexpr int MULTI_K = 4;
+size_t multi_smem_bytes(const LoopParams& P, bool f64);
+int multi_max_batch();
+cudaError_t launch_multi_loop(const LoopParams& P, bool f64, int threads, cudaStream_t st);
+int multi_max_cluster(bool f64, bool srec, int TW, int threads, size_t smem);
 
 // alternative loop kernel (mplean.cu): geometry once per CTA into row descriptors,
 // work items = row segments; selected with profile-mode bit 2

@@ -73,7 +73,8 @@ struct mpgabor {
   int cluster_req = 0, threads = 512, TW_req = 0, srec_req = 0;  // 0 = automatic
   int TW = 64, srec = 0;
   int run_threads = 512;  // threads of the planned loop launch
-  int kind = 0;           // loop kernel: 0 mploop.cu, 1 mplean.cu
+  int batch = 0;          // candidates per round: 0 auto (multi-selection, multi_max_batch()), 1 one selection
+  int kind = 2;           // loop kernel: 0 mploop.cu, 1 mplean.cu, 2 mpmulti.cu
 
   // per-length layout
   int64_t L = -1, Ls_cached = -1;
@@ -83,7 +84,7 @@ struct mpgabor {
   DevBuf d_own;
   int64_t grid_elems = 0, total_tiles = 0, Lc = 0, P_R = 0;
   LoopParams lp{};
-  DevBuf d_geo, grid, rec, xp, partial, flag, E0, result;
+  DevBuf d_geo, grid, rec, xp, partial, flag, E0, result, backup;
 
   // synth / host-api scratch
   DevBuf sol, frames, hx, hatoms, henergy, hy;
@@ -196,7 +197,7 @@ extern "C" void mpgabor_destroy(mpgabor* h) {
     cudaSetDevice(h->device);
     for (DevBuf* b : {&h->tw, &h->roots, &h->win, &h->kern, &h->boxcopy, &h->d_pairs, &h->rho, &h->rho_meta,
                       &h->Hscratch, &h->mxbox, &h->d_geo, &h->grid, &h->rec, &h->xp, &h->partial, &h->flag,
-                      &h->E0, &h->result, &h->sol, &h->frames, &h->hx, &h->hatoms, &h->henergy, &h->hy, &h->prof, &h->d_own, &h->trace})
+                      &h->E0, &h->result, &h->sol, &h->frames, &h->hx, &h->hatoms, &h->henergy, &h->hy, &h->prof, &h->d_own, &h->trace, &h->backup})
       b->release();
     for (auto e : h->ev)
       if (e) cudaEventDestroy(e);
@@ -514,11 +515,13 @@ static size_t plan_loop(mpgabor* h, int TW, int srec, int C) {
     n = (n + 31) / 32;
   }
   P.nlev = nl;
-  // loop kernel: 0 = mploop.cu (default), 1 = mplean.cu (profile-mode bit 2)
-  const int kind = (h->prof_mode & 4) ? 1 : 0;
+  // loop kernel: 2 = mpmulti.cu (default), 0 = mploop.cu (batch 1), 1 = mplean.cu (profile-mode bit 2)
+  const int kind = (h->prof_mode & 4) ? 1 : (h->batch == 1 ? 0 : 2);
   h->kind = kind;
   h->run_threads = h->threads;
-  P.smem_bytes = kind == 1 ? lean_smem_bytes(P, h->f64()) : loop_smem_bytes(P, h->f64());
+  P.spec = h->batch == 0 ? multi_max_batch() : h->batch;
+  P.smem_bytes = kind == 1 ? lean_smem_bytes(P, h->f64())
+                           : (kind == 2 ? multi_smem_bytes(P, h->f64()) : loop_smem_bytes(P, h->f64()));
   return P.smem_bytes;
 }
 
@@ -558,8 +561,9 @@ static int ensure_layout(mpgabor* h, int64_t Ls) {
         why = "shared memory " + std::to_string(smem) + " B";
         break;  // smaller clusters need more per-CTA memory
       }
-      const int cmax = h->kind == 1 ? lean_max_cluster(h->f64(), c.srec, c.TW, h->run_threads, smem)
-                                    : loop_max_cluster(h->f64(), c.srec, c.TW, h->run_threads, smem);
+      const int cmax = h->kind == 1   ? lean_max_cluster(h->f64(), c.srec, c.TW, h->run_threads, smem)
+                       : h->kind == 2 ? multi_max_cluster(h->f64(), c.srec, c.TW, h->run_threads, smem)
+                                      : loop_max_cluster(h->f64(), c.srec, c.TW, h->run_threads, smem);
       if (cmax >= C) {
         ok = true;
         break;
@@ -588,6 +592,23 @@ static int ensure_layout(mpgabor* h, int64_t Ls) {
   TRY_CUDA(h, h->flag.ensure(sizeof(int)));
   TRY_CUDA(h, h->E0.ensure(sizeof(double)));
   TRY_CUDA(h, h->result.ensure(sizeof(LoopResult)));
+  if (h->kind == 2) {
+    // roll-back backups: per CTA and round at most spec x max_u sum_v (rows/C + 1) x (hull tiles)
+    // items (rows = alignment-class sub-box rows, hull tiles <= cols/TW + 1)
+    int64_t per_atom = 0;
+    for (int u = 0; u < W; ++u) {
+      int64_t s = 0;
+      for (int v = 0; v < W; ++v) {
+        const PairGeo& pg = h->pairs[u * W + v];
+        const int64_t rows = (pg.nnu + pg.s_n - 1) / pg.s_n, cols = (pg.nmu + pg.s_m - 1) / pg.s_m;
+        const int64_t tiles = std::min<int64_t>(h->geo[v].T, (cols + h->TW - 1) / h->TW + 1);
+        s += ((rows + P.C - 1) / P.C + 1) * tiles;
+      }
+      per_atom = std::max(per_atom, s);
+    }
+    P.bk_cap = per_atom * P.spec;
+    TRY_CUDA(h, h->backup.ensure(h->celem() * (size_t)h->TW * P.bk_cap * P.C));
+  }
   h->L = L;
   h->lay_TW = h->TW;
   return MPG_OK;
@@ -692,8 +713,11 @@ extern "C" int mpgabor_run(mpgabor* h, const double* x_dev, int64_t Ls, int64_t 
     P.prof = h->prof.as<long long>();
   }
   TRY_CUDA(h, cudaEventRecord(h->ev[3], st));
+  P.backup = h->backup.p;
   if (h->kind == 1)
     TRY_LAUNCH(h, 1, launch_lean_loop(P, h->f64(), h->run_threads, st));
+  else if (h->kind == 2)
+    TRY_LAUNCH(h, 1, launch_multi_loop(P, h->f64(), h->run_threads, st));
   else
     TRY_LAUNCH(h, 1, launch_mp_loop(P, h->f64(), h->run_threads, st));
   TRY_CUDA(h, cudaEventRecord(h->ev[4], st));
@@ -710,6 +734,7 @@ extern "C" int mpgabor_run(mpgabor* h, const double* x_dev, int64_t Ls, int64_t 
   res->cluster = h->lay_C;
   res->E0 = E0;
   res->E_final = lr.E_final;
+  res->rounds = h->kind == 2 ? lr.rounds : lr.n_done + 1;
   return MPG_OK;
 }
 
@@ -726,6 +751,15 @@ extern "C" int mpgabor_residual(mpgabor* h, double* out_dev, void* stream) {
     TRY_LAUNCH(h, 1, launch_grid_export<float>(h->grid.as<float2>(), h->d_geo.as<DictGeo>(), h->W, h->P_R,
                                           reinterpret_cast<double2*>(out_dev), st));
   TRY_CUDA(h, cudaStreamSynchronize(st));
+  return MPG_OK;
+}
+
+extern "C" int mpgabor_set_batch(mpgabor* h, int32_t max_batch) {
+  if (!h) return MPG_EINVAL;
+  if (max_batch < 0 || max_batch > multi_max_batch())
+    return h->fail(MPG_EINVAL, "max_batch must be in [0, " + std::to_string(multi_max_batch()) + "]");
+  if (max_batch != h->batch) h->L = -1;  // the loop kernel and its buffers are re-planned
+  h->batch = max_batch;
   return MPG_OK;
 }
 

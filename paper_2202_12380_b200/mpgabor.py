@@ -35,7 +35,7 @@ class mpg_dict(ctypes.Structure):
 class mpg_result(ctypes.Structure):
     _fields_ = [("n_atoms", ctypes.c_int64), ("L_pad", ctypes.c_int64),
                 ("stop_reason", ctypes.c_int32), ("cluster", ctypes.c_int32),
-                ("E0", ctypes.c_double), ("E_final", ctypes.c_double)]
+                ("E0", ctypes.c_double), ("E_final", ctypes.c_double), ("rounds", ctypes.c_int64)]
 
 
 class MpgError(RuntimeError):
@@ -63,6 +63,7 @@ _SIGS = {
     "mpgabor_decompose_host": ([_P, _P, _I64, _I64, ctypes.c_double, _P, _P, _P,
                                 ctypes.POINTER(mpg_result), _P], ctypes.c_int),
     "mpgabor_set_launch": ([_P, _I32, _I32, _I32, _I32], ctypes.c_int),
+    "mpgabor_set_batch": ([_P, _I32], ctypes.c_int),
     "mpgabor_launch_info": ([_P, ctypes.POINTER(_I32), ctypes.POINTER(_I32), ctypes.POINTER(_I32),
                              ctypes.POINTER(_I32), ctypes.POINTER(_I64)], ctypes.c_int),
     "mpgabor_kernel_stats": ([_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I64)],
@@ -169,6 +170,10 @@ def mpgabor_set_launch(h, cluster=0, threads=0, tile_width=0, records=0):
     _check(h, _lib.mpgabor_set_launch(h, int(cluster), int(threads), int(tile_width), int(records)))
 
 
+def mpgabor_set_batch(h, max_batch):
+    _check(h, _lib.mpgabor_set_batch(h, int(max_batch)))
+
+
 def mpgabor_launch_info(h):
     c, t, tw, r = _I32(), _I32(), _I32(), _I32()
     sm = _I64()
@@ -255,6 +260,7 @@ class RunOutput:
     cluster: int
     coef: object = None    # torch complex128 [P_R] on device (or None)
     atoms_dev: object = None
+    rounds: int = 0        # persistent-loop rounds (multi-selection)
 
     @property
     def n(self):
@@ -303,6 +309,9 @@ class MPGabor:
     def launch_info(self):
         return mpgabor_launch_info(self.h)
 
+    def set_batch(self, max_batch):
+        mpgabor_set_batch(self.h, max_batch)
+
     def alloc(self, maxit, Ls, want_coef=False):
         torch = self.torch
         atoms = torch.empty(max(int(maxit), 1) * ATOM_DTYPE.itemsize, dtype=torch.uint8, device="cuda")
@@ -327,7 +336,7 @@ class MPGabor:
         at = np.frombuffer(atoms[: n * ATOM_DTYPE.itemsize].cpu().numpy().tobytes(), dtype=ATOM_DTYPE)
         en = energy[: n + 1].cpu().numpy()
         return RunOutput(at, en, res.stop_reason, res.E0, res.L_pad, res.cluster,
-                         coef.view(torch.complex128) if coef is not None else None, atoms)
+                         coef.view(torch.complex128) if coef is not None else None, atoms, res.rounds)
 
     def synth(self, atoms_dev, n_atoms, Ls, stream=None):
         torch = self.torch

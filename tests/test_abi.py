@@ -42,7 +42,7 @@ def test_library_exports_every_declared_symbol(mpg):
 def test_struct_layouts(mpg):
     assert ctypes.sizeof(mpg.mpg_dict) == 16
     assert mpg.ATOM_DTYPE.itemsize == 32            # mpg_atom
-    assert ctypes.sizeof(mpg.mpg_result) == 40
+    assert ctypes.sizeof(mpg.mpg_result) == 48
 
 
 @pytest.mark.parametrize("dicts,code", [
@@ -83,6 +83,12 @@ def test_precision_and_state_errors(mpg):
         with pytest.raises(mpg.MpgError):
             mpg.mpgabor_set_launch(h, 0, 0, 48, 0)
         mpg.mpgabor_set_launch(h, 4, 256, 32, 1)
+        for bad in (-1, 9):
+            with pytest.raises(mpg.MpgError) as e:
+                mpg.mpgabor_set_batch(h, bad)
+            assert "EINVAL" in str(e.value)
+        for ok in (0, 1, 4, 8):
+            mpg.mpgabor_set_batch(h, ok)
         with pytest.raises(mpg.MpgError) as e:
             mpg.mpgabor_kernel_stats(h)             # before mpgabor_kernels
         assert "ESTATE" in str(e.value)
