@@ -203,11 +203,18 @@ int mpgabor_residual(mpgabor* h, double* out_dev, void* cuda_stream);
  * of such a run are NOT a decomposition and must only be used for timing. */
 int mpgabor_set_profile(mpgabor* h, int32_t mode);
 
-/* cycles (host int64[8]) of the last run with mode bit0, summed over the
- * iterations on CTA 0 / thread 0: [0] wait for the C roots (mailbox barrier),
- * [1] selection + scalar step, [2] block barrier after selection, [3] own
- * update work, [4] block barrier after the update, [5] level-1 refresh +
- * barrier, [6] upper levels + root publication; [7] iterations. */
+/* cycles (host int64[32]) of the last run with mode bit0, summed over the
+ * iterations on CTA 0 / thread 0.  One-selection loop (mpgabor_set_batch 1):
+ * [0] wait for the C roots (mailbox barrier), [1] selection + scalar step,
+ * [2] block barrier after selection, [3] own update work, [4] block barrier
+ * after the update, [5] level-1 refresh + barrier, [6] upper levels + root
+ * publication; [7] iterations.  Multi-selection loop: [0] wait for the
+ * messages, [1] verification, [2] barrier, [3] list ranking, [4] barrier,
+ * [5] window geometry + scalar steps, [6] barrier, [7] pairwise masks,
+ * [8] barrier, [9] walk + item bases, [10] barrier, [11] own items,
+ * [12] barrier + level-1 refresh + barrier, [13] upper levels + top-K,
+ * [14] message push; [15] rounds; [16..19] own items: set-up, loads and
+ * update, tile bookkeeping, items processed. */
 int mpgabor_last_profile(const mpgabor* h, int64_t* cycles);
 
 /* Event timeline of iterations [it0, it0+n) of the next runs (n = 0 disables):

@@ -1,0 +1,207 @@
+// loopcore.cuh -- device building blocks shared by the persistent MP loop kernels
+// (mploop.cu: one selection per iteration; mpmulti.cu: exact multi-selection rounds).
+//
+//   * ScoreOps      |c|^2 without FMA contraction (both sides of the argmax parity,
+//                   DESIGN.md §2 note under Z21)
+//   * VGeo/vgeo()   the Alg. 3 index sets of one target dictionary v
+//                   for a selected atom (u, k, j): alignment class of the kernel box,
+//                   first frame / bin, folded bin hull in tiles, this CTA's rows
+//   * mailbox       st.async into remote shared memory + mbarrier complete_tx
+//   * warp_node     32-ary max-tree node re-reduction
+#pragma once
+#include "argmax.cuh"
+#include "launch.h"
+
+namespace mpcore {
+
+template <typename R>
+struct ScoreOps;
+template <>
+struct ScoreOps<double> {
+  static __device__ __forceinline__ double score(double re, double im) {
+    return __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im));
+  }
+};
+template <>
+struct ScoreOps<float> {
+  static __device__ __forceinline__ float score(float re, float im) {
+    return __fadd_rn(__fmul_rn(re, re), __fmul_rn(im, im));
+  }
+};
+
+// Correctly rounded arithmetic without FMA contraction, so that every loop kernel
+// (and the oracle, compiled with -ffp-contract=off) rounds the update identically.
+template <typename R>
+struct Ar;
+template <>
+struct Ar<double> {
+  static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+  static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+  static __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+};
+template <>
+struct Ar<float> {
+  static __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
+  static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+  static __device__ __forceinline__ float sub(float a, float b) { return __fsub_rn(a, b); }
+};
+
+// z0 = c~ omega (fp64, then rounded to R) for one kernel row (Eq. (15))
+template <typename C2, typename R>
+__device__ __forceinline__ C2 row_z0(double tre, double tim, double2 w) {
+  C2 z;
+  z.x = (R)__dsub_rn(__dmul_rn(tre, w.x), __dmul_rn(tim, w.y));
+  z.y = (R)__dadd_rn(__dmul_rn(tre, w.y), __dmul_rn(tim, w.x));
+  return z;
+}
+
+// One target bin of Alg. 3 with the fold rule (Z14): z = z0 h; the direct term
+// c -= z_d and the conjugate term c -= conj(z_c), in ascending source-column order.
+template <typename R, typename C2>
+__device__ __forceinline__ C2 fold_update(C2 c, C2 z0, C2 hd, C2 hc, bool fd, bool fc, bool cfirst) {
+  using A = Ar<R>;
+  const R zdx = A::sub(A::mul(z0.x, hd.x), A::mul(z0.y, hd.y));
+  const R zdy = A::add(A::mul(z0.x, hd.y), A::mul(z0.y, hd.x));
+  const R zcx = A::sub(A::mul(z0.x, hc.x), A::mul(z0.y, hc.y));
+  const R zcy = A::add(A::mul(z0.x, hc.y), A::mul(z0.y, hc.x));
+  if (fc && cfirst) {
+    c.x = A::sub(c.x, zcx);
+    c.y = A::add(c.y, zcy);
+  }
+  if (fd) {
+    c.x = A::sub(c.x, zdx);
+    c.y = A::sub(c.y, zdy);
+  }
+  if (fc && !cfirst) {
+    c.x = A::sub(c.x, zcx);
+    c.y = A::add(c.y, zcy);
+  }
+  return c;
+}
+
+struct VGeo {           // update geometry for one target dictionary v, seen from this CTA
+  long long kbase;      // first kernel entry of the alignment class
+  int nr, nc;           // rows (frames) and columns (bins) of the class sub-box
+  int n0, q0;           // first target frame, first target bin (before folding)
+  int t0, Tr;           // first tile and tile count of the folded bin hull
+  int rA, rhoA, cntA;   // rows [0, rA) do not wrap; owned rows rhoA + i*C, i < cntA
+  int rhoB, cntB;       // rows [rA, nr) wrap to frame 0..; owned rows rA + rhoB + i*C, i < cntB
+  int base, nitems;     // this CTA's items of v: (cntA + cntB) * Tr tiles
+  int rr0, rrstep;      // modulation exponent of row 0 and its per-row step (mod R)
+  int pad;
+};
+
+// fold(Q) = min(Q mod M, M - Q mod M) over the run Q = q0 .. q0+nc-1 (q0 in [0,M)):
+// hull [bmin, bmax] of the reduced bins that receive a direct or conjugate term
+__device__ __forceinline__ void target_hull(int q0, int nc, int M, int& bmin, int& bmax) {
+  const int qa = q0, qb = q0 + nc - 1;
+  const int half = M >> 1;
+  const int ra = qa & (M - 1), rb = qb & (M - 1);
+  const int fa = ra <= half ? ra : M - ra, fb = rb <= half ? rb : M - rb;
+  const bool trough = (qa == 0) || (qb >= M);
+  const bool peak = (qa <= half && qb >= half) || (qb >= M + half);
+  bmin = trough ? 0 : min(fa, fb);
+  bmax = peak ? half : max(fa, fb);
+}
+
+// Update geometry of target dictionary v for the atom (u, k, j) of dictionary u
+// (SURVEY O7e / Alg. 3): the alignment class (o_n, o_m) of the (u, v) kernel box,
+// its nr x nc sub-box, the first target frame n0 and bin q0, the folded bin hull
+// in tiles [t0, t0 + Tr), the rows owned by CTA `rank` of a C-CTA cluster and the
+// modulation exponents.  Every stride is a power of two (shift/mask arithmetic).
+// Returns this CTA's item count (rows x hull tiles).
+template <int LGTW>
+__device__ __forceinline__ int vgeo(const PairGeo& pg, const DictGeo& du, const DictGeo& dv, int k, int j, int rank,
+                                    int C, int lgC, VGeo& g) {
+  const int lgac = ilog2(pg.a_c), lgsm = ilog2(pg.s_m), lgsn = ilog2(pg.s_n);
+  const int kp = k << (ilog2(pg.M_c) - ilog2(du.M));                       // k' = k M_c/M_u
+  const int on = (-(j << (ilog2(du.a) - lgac)) - pg.nu_lo) & (pg.s_n - 1);
+  const int om = (-kp - pg.mu_lo) & (pg.s_m - 1);
+  g.nr = on < pg.nnu ? (pg.nnu - on + pg.s_n - 1) >> lgsn : 0;
+  g.nc = om < pg.nmu ? (pg.nmu - om + pg.s_m - 1) >> lgsm : 0;
+  const int tnum = (j << ilog2(du.a)) + ((pg.nu_lo + on) << lgac);          // divisible by a_v
+  int n0 = tnum >> ilog2(dv.a);
+  if (n0 < 0) n0 += dv.N;
+  if (n0 >= dv.N) n0 -= dv.N;
+  g.n0 = n0;
+  g.q0 = ((kp + pg.mu_lo + om) >> lgsm) & (dv.M - 1);
+  g.kbase = pg.koff + (long long)(on * (pg.nnu >> lgsn) + min(on, pg.nnu & (pg.s_n - 1))) * pg.nmu +
+            (long long)g.nr * (om * (pg.nmu >> lgsm) + min(om, pg.nmu & (pg.s_m - 1)));
+  int bmin = 0, bmax = 0;
+  if (g.nc > 0) target_hull(g.q0, g.nc, dv.M, bmin, bmax);
+  g.t0 = bmin >> LGTW;
+  g.Tr = (bmax >> LGTW) - g.t0 + 1;
+  // rows owned by this CTA: frame f = frame_off_v + n belongs to CTA f mod C
+  g.rA = min(g.nr, dv.N - n0);
+  g.rhoA = (rank - (dv.frame_off + n0)) & (C - 1);
+  g.cntA = g.rhoA < g.rA ? ((g.rA - 1 - g.rhoA) >> lgC) + 1 : 0;
+  const int nB = g.nr - g.rA;
+  g.rhoB = (rank - dv.frame_off) & (C - 1);
+  g.cntB = (nB > 0 && g.rhoB < nB) ? ((nB - 1 - g.rhoB) >> lgC) + 1 : 0;
+  const int nitems = g.nc > 0 ? (g.cntA + g.cntB) * g.Tr : 0;
+  g.rr0 = (kp * (pg.nu_lo + on)) & (pg.R - 1);
+  g.rrstep = (kp << lgsn) & (pg.R - 1);
+  g.nitems = nitems;
+  g.base = 0;
+  g.pad = 0;
+  return nitems;
+}
+
+// ---- cluster mailbox: st.async into remote shared memory + mbarrier complete_tx ----
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t mapa(uint32_t a, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arm(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void st_async16(uint32_t raddr, uint32_t rbar, uint4 v) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(raddr),
+               "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(rbar)
+               : "memory");
+}
+template <typename R>
+__device__ __forceinline__ void push_record(const Rec<R>& r, uint32_t raddr, uint32_t rbar) {
+  const uint4* w = reinterpret_cast<const uint4*>(&r);
+#pragma unroll
+  for (int i = 0; i < (int)(sizeof(Rec<R>) / 16); ++i) st_async16(raddr + 16 * i, rbar, w[i]);
+}
+
+// one warp re-reduces node `node` of a level from its (up to) 32 children
+template <typename R>
+__device__ __forceinline__ void warp_node(const Rec<R>* child, long long nchild, int node, Rec<R>* out, int lane) {
+  const long long c = (long long)node * 32 + lane;
+  const Rec<R> r = c < nchild ? child[c] : empty_rec(R(0));
+  R s;
+  uint32_t p;
+  const int wl = warp_argmax(r.s, r.p, s, p);
+  if (lane == wl) out[node] = r;
+}
+
+// 32-bit conservative key of a score for the multi-selection verification:
+// fp32 -- the exact bit pattern; fp64 -- the upper word (the score rounded down
+// to 20 mantissa bits).  key(s1) < key(s2) implies s1 < s2.
+__device__ __forceinline__ uint32_t score_key(double s) {
+  return (uint32_t)((unsigned long long)__double_as_longlong(s) >> 32);
+}
+__device__ __forceinline__ uint32_t score_key(float s) { return (uint32_t)__float_as_int(s); }
+// exact 64-bit order key of a (non-negative) score
+__device__ __forceinline__ uint64_t skey64(double s) { return (uint64_t)__double_as_longlong(s); }
+__device__ __forceinline__ uint64_t skey64(float s) { return (uint64_t)(uint32_t)__float_as_int(s) << 32; }
+
+}  // namespace mpcore

@@ -320,9 +320,7 @@ __global__ void __launch_bounds__(512, 1) mp_loop_kernel(const LoopParams P) {
         // modulation omega_R^{(k' nu) mod R} of this row (Eq. (15))
         const int rr = (g.rr0 + r * g.rrstep) & (pg.R - 1);
         const double2 w = roots[rr * pg.rstep];
-        C2 z0;
-        z0.x = (R)(tre * w.x - tim * w.y);
-        z0.y = (R)(tre * w.y + tim * w.x);
+        const C2 z0 = row_z0<C2, R>(tre, tim, w);
         const C2* hrow = kern + g.kbase + (long long)r * g.nc;
         C2* row = grid + dv.grid_off + (long long)nrow * dv.stride;
         const int Mv = dv.M;
@@ -347,22 +345,8 @@ __global__ void __launch_bounds__(512, 1) mp_loop_kernel(const LoopParams P) {
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch) {
           const int bin = t * TW + ch * 32 + lane;
-          C2 c = cv[ch];
-          // z = z0 h;  direct: c -= z;  conjugate: c -= conj(z)
-          const R zdx = z0.x * hd[ch].x - z0.y * hd[ch].y, zdy = z0.x * hd[ch].y + z0.y * hd[ch].x;
-          const R zcx = z0.x * hc[ch].x - z0.y * hc[ch].y, zcy = z0.x * hc[ch].y + z0.y * hc[ch].x;
-          if (fc[ch] && cfirst[ch]) {
-            c.x -= zcx;
-            c.y += zcy;
-          }
-          if (fd[ch]) {
-            c.x -= zdx;
-            c.y -= zdy;
-          }
-          if (fc[ch] && !cfirst[ch]) {
-            c.x -= zcx;
-            c.y += zcy;
-          }
+          // z = z0 h;  direct: c -= z;  conjugate: c -= conj(z)   (fold rule Z14)
+          const C2 c = fold_update<R>(cv[ch], z0, hd[ch], hc[ch], fd[ch], fc[ch], cfirst[ch]);
           if (bin < dv.MR) {
             if (fd[ch] || fc[ch]) row[bin] = c;
             const R s = ScoreOps<R>::score(c.x, c.y);

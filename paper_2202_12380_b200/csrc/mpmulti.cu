@@ -1,0 +1,1042 @@
+// mpmulti.cu -- exact multi-selection rounds of the coefficient-domain MP loop
+// (DESIGN.md §8).
+//
+// The sequential loop of Alg. 1 (recursion Eq. (9)) spends
+// almost all of its time in the dependency chain select -> update -> refresh ->
+// select (mploop.cu).  Eq. (16)'s locality makes most
+// consecutive selections independent: an update only changes the coefficients
+// inside the kernel footprint of the selected atom.  A round therefore picks up
+// to B atoms at once and proves, one round later, that they are exactly the
+// atoms the sequential loop would have selected:
+//
+//   tiles(p)  the set of tiles (TW bins of one frame row) the update of atom p
+//             reads and writes: in every target dictionary v the rows of the
+//             kernel's alignment-class sub-box times the folded bin hull.
+//   Round: p_1 = global argmax.  p_i (i >= 2) = the best coefficient outside
+//   X_i = tiles(p_1) u ... u tiles(p_{i-1}) in the state before the round,
+//   taken only if tiles(p_i) is disjoint from X_i.  All updates are applied
+//   (they touch disjoint tiles, so each coefficient receives exactly the
+//   arithmetic of the sequential loop), every CTA records per candidate the
+//   largest post-update score over its tiles, and p_i is *accepted* iff that
+//   maximum over X_i is below |c(p_i)|^2.  Then p_i is the sequential argmax
+//   after p_1..p_{i-1}: outside X_i nothing changed and p_i is the best there,
+//   inside X_i every value is smaller.  c(p_i) is unchanged by the earlier
+//   updates (p_i is outside X_i), so c~ and E~ (Eqs. (19)-(20)) are the
+//   sequential ones.  The comparison uses a conservative 32-bit score key
+//   (equality rejects), so a rejection never breaks exactness.
+//   Rejected candidates are rolled back bit-exactly in the next round from a
+//   backup of their tiles (a copy, not an inverse update), and that round does
+//   no selection.
+//
+// The candidates come from per-CTA top-K lists: at the end of a round every CTA
+// extracts its K best tile records (exact, from its 32-ary max tree) and pushes
+// them, with its per-candidate maxima, into every CTA's mailbox (st.async +
+// mbarrier complete_tx, as in mploop.cu).  Every CTA then runs the same
+// deterministic merge/walk: entries in descending (score, -index) order; an
+// entry whose tile lies in X is skipped; passing the K-th entry of a CTA's list
+// ends the walk (that CTA's unlisted tiles are unknown); the walk also ends at
+// the first candidate whose tiles meet X, at a stop rule (Z15) or after B picks.
+//
+// Frame ownership, tile records, node tree and the per-tile update arithmetic
+// are those of mploop.cu; the run is deterministic and its atom sequence is
+// identical to the one-selection loop.
+#include <cooperative_groups.h>
+#include "loopcore.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace {
+
+using namespace mpcore;
+
+constexpr int NE = 16;    // walk window: best merged list entries considered per round
+constexpr int BMAX = 8;   // candidates per round (upper bound; LoopParams::spec lowers it)
+
+template <typename R, int K>
+struct Msg {              // published by every CTA to every CTA at the end of a round
+  Rec<R> list[K];         // its K best tile records, (score desc, index asc)
+  uint32_t vkey[BMAX];    // per candidate: max score key over the candidate's tiles owned by the CTA
+  uint2 rect[K * 16];     // packed tiles(list[i]) in target dictionary v at [i * W + v] (W <= 16);
+                          // only the first K * W entries are pushed
+};
+template <typename R, int K>
+__host__ __device__ constexpr size_t msg_head() {
+  return sizeof(Rec<R>) * K + sizeof(uint32_t) * BMAX;
+}
+
+struct Ent {              // one merged list entry of the walk window
+  double tre, tim, Et;    // c~ (Eq. (19)) and E~ (Eq. (20)) if selected
+  uint32_t key;           // score_key of |c|^2
+  int u, k, j;            // dictionary, bin, frame
+  int tile;               // k / TW
+  int last;               // 1: the K-th entry of its CTA's list
+  int pos;                // 1: |c|^2 > 0 and a real record
+  int selfc;              // self-conjugate (k = 0 or M_u/2, Z13)
+};
+
+struct St {               // round state (shared memory)
+  double E;               // E_k after the accepted atoms
+  long long it;           // accepted atoms
+  double Enext[BMAX];     // E after candidate g
+  int G;                  // candidates of the round just run (verified by the next round)
+  int mode;               // 0 select, 1 roll back candidates rb_from..G-1
+  int rb_from;
+  int stop;
+  uint32_t ckey[BMAX];    // score key of candidate g
+  alignas(16) int ibase[BMAX * 16 + 4];  // this CTA's items (tile pairs) before (g, v), index g * 16 + v
+  alignas(16) int tbase[BMAX * 16 + 4];  // this CTA's tiles (backup slots) before (g, v)
+};
+
+struct Smem {
+  size_t mbar, mail, mymsg, trec, lev, ent, egeo, wmask, st, vkey, sorted, tk, dwoff, dirty, pairs, dicts, own, roots,
+      rho, rho_meta, total;
+};
+
+__host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+__host__ __device__ inline int dirty_words(const LoopParams& P) {
+  int w = 0;
+  for (int l = 0; l < P.nlev; ++l) w += (P.lev_n[l] + 31) / 32;
+  return w;
+}
+
+__host__ __device__ inline Smem smem_layout(const LoopParams& P, size_t recsz, size_t msgsz) {
+  Smem s;
+  int levtot = 0;
+  for (int l = 0; l < P.nlev; ++l) levtot += P.lev_n[l];
+  size_t o = 0;
+  s.mbar = o;
+  o += 32;
+  s.mail = o;
+  o += 2 * MAX_CLUSTER * msgsz;
+  s.mymsg = o;
+  o += msgsz;
+  s.trec = o;
+  o += P.srec ? (size_t)P.Lc * recsz : 0;
+  s.lev = o;
+  o += (size_t)levtot * recsz;
+  o = align_up(o, 16);
+  s.ent = o;
+  o += sizeof(Ent) * BMAX;
+  o = align_up(o, 16);
+  s.egeo = o;
+  o += sizeof(VGeo) * BMAX * P.W;
+  o = align_up(o, 16);
+  s.wmask = o;
+  o += sizeof(uint32_t) * 2 * NE;
+  o = align_up(o, 16);
+  s.st = o;
+  o += sizeof(St);
+  o = align_up(o, 16);
+  s.vkey = o;
+  o += sizeof(uint32_t) * BMAX;
+  s.sorted = o;
+  o += sizeof(int) * NE;
+  s.tk = o;
+  o += sizeof(int) * 64;
+  s.dwoff = o;
+  o += sizeof(int) * (MAX_LEVELS + 1);
+  o = align_up(o, 16);
+  s.dirty = o;
+  o += sizeof(uint32_t) * dirty_words(P);
+  o = align_up(o, 16);
+  s.pairs = o;
+  o += sizeof(PairGeo) * P.W * P.W;
+  o = align_up(o, 16);
+  s.dicts = o;
+  o += sizeof(DictGeo) * P.W;
+  o = align_up(o, 16);
+  s.own = o;
+  o += sizeof(OwnGeo) * P.W;
+  o = align_up(o, 16);
+  s.roots = o;
+  o += P.Rmax <= 4096 ? sizeof(double2) * P.Rmax : 0;
+  s.rho = o;
+  o += sizeof(RhoEnt) * P.rho_total;
+  s.rho_meta = o;
+  o += sizeof(int) * 3 * P.W;
+  s.total = align_up(o, 16);
+  return s;
+}
+
+// One warp, one candidate per lane (64-bit order key, index p; empty: 0 / NO_INDEX):
+// K pops of the warp-wide best (key desc, index asc), resolved on the upper key word
+// and only on ties on the lower word / the index.  The winner of pop t writes
+// out[t] = its id (-1 when empty).
+template <int K>
+__device__ __forceinline__ void warp_pop_k(uint64_t key, uint32_t p, int id, int* out, int lane) {
+#pragma unroll
+  for (int t = 0; t < K; ++t) {
+    const uint32_t hi = (uint32_t)(key >> 32), lo = (uint32_t)key;
+    const uint32_t mhi = __reduce_max_sync(0xffffffffu, hi);
+    unsigned m = __ballot_sync(0xffffffffu, hi == mhi);
+    if (m & (m - 1)) {
+      const uint32_t mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+      m = __ballot_sync(0xffffffffu, hi == mhi && lo == mlo);
+      if (m & (m - 1)) {
+        const bool in = (m >> lane) & 1u;
+        const uint32_t mp = __reduce_min_sync(0xffffffffu, in ? p : NO_INDEX);
+        m = __ballot_sync(0xffffffffu, in && p == mp);
+      }
+    }
+    if (lane == __ffs(m) - 1) {
+      out[t] = p == NO_INDEX ? -1 : id;
+      key = 0;
+      p = NO_INDEX;
+    }
+  }
+}
+
+// Exact top-K tiles of this CTA down its node tree, by all warps: at every level
+// the candidates are the children of the previous level's K winners (all nodes at
+// the top level; the top-K nodes of a level contain the top-K of the level below),
+// split in chunks of 32; warp q pops the K best of chunk q, warp 0 pops the K best
+// of the chunk winners.  Leaves the tile ids (-1 = none) in tk[0..K-1]; tk[16..]
+// holds the chunk winners.  Needs a barrier before; ends with one.
+template <typename R, int K>
+__device__ __forceinline__ void cta_topk(const LoopParams& P, const Rec<R>* lev, const Rec<R>* trec, int* tk,
+                                         int lane, int warp) {
+  static_assert(K * 8 <= 32, "the merge holds 8 chunks x K winners in one warp");
+  int* part = tk + 16;
+  const int top = P.nlev - 1;
+  for (int l = top; l >= -1; --l) {
+    const bool first = l == top;
+    const int count = l >= 0 ? P.lev_n[l] : (int)P.Lc;
+    const Rec<R>* arr = l >= 0 ? lev + P.lev_off[l] : trec;
+    const int nq = first ? (count + 31) >> 5 : K;
+    if (warp < nq) {
+      int id = first ? warp * 32 + lane : (tk[warp] >= 0 ? tk[warp] * 32 + lane : -1);
+      uint64_t key = 0;
+      uint32_t p = NO_INDEX;
+      if (id >= 0 && id < count) {
+        key = skey64(arr[id].s);
+        p = arr[id].p;
+      } else {
+        id = -1;
+      }
+      warp_pop_k<K>(key, p, id, part + warp * K, lane);
+    }
+    __syncthreads();
+    if (warp == 0) {
+      int id = lane < nq * K ? part[lane] : -1;
+      uint64_t key = 0;
+      uint32_t p = NO_INDEX;
+      if (id >= 0) {
+        key = skey64(arr[id].s);
+        p = arr[id].p;
+      }
+      warp_pop_k<K>(key, p, id, tk, lane);
+    }
+    __syncthreads();
+  }
+}
+
+// global reduced index p -> dictionary u, bin k, frame j (p = off_u + j * M_R,u + k, Z10)
+__device__ __forceinline__ void decode_p(uint32_t p, const DictGeo* sd, int W, int& u, int& k, int& j) {
+  u = 0;
+  for (int w = 1; w < W; ++w) u += (uint32_t)sd[w].off <= p ? 1 : 0;
+  const uint32_t q = p - (uint32_t)sd[u].off;
+  const int MR = sd[u].MR;
+  j = (int)(q / (uint32_t)MR);
+  k = (int)(q - (uint32_t)j * (uint32_t)MR);
+}
+
+// packed rect of the tiles an update touches in one target dictionary:
+// x = first row n0 | rows nr << 20 (rows [n0, n0+nr) mod N), y = first tile t0 | tiles Tr << 16
+__device__ __forceinline__ uint2 pack_rect(const VGeo& g) {
+  const bool empty = g.nr == 0 || g.nc == 0;
+  return make_uint2(empty ? 0u : ((uint32_t)g.n0 | ((uint32_t)g.nr << 20)), (uint32_t)g.t0 | ((uint32_t)g.Tr << 16));
+}
+__device__ __forceinline__ bool rects_meet(uint2 a, uint2 b, int N) {
+  const int an = a.x & 0xFFFFF, ar = a.x >> 20, bn = b.x & 0xFFFFF, br = b.x >> 20;
+  const int at = a.y & 0xFFFF, aT = a.y >> 16, bt = b.y & 0xFFFF, bT = b.y >> 16;
+  int d1 = bn - an, d2 = an - bn;
+  d1 += d1 < 0 ? N : 0;
+  d2 += d2 < 0 ? N : 0;
+  return (at < bt + bT) & (bt < at + aT) & ((d1 < ar) | (d2 < br)) & (ar > 0) & (br > 0);
+}
+__device__ __forceinline__ bool rect_has(uint2 a, int n, int t, int N) {
+  const int an = a.x & 0xFFFFF, ar = a.x >> 20, at = a.y & 0xFFFF, aT = a.y >> 16;
+  int d = n - an;
+  d += d < 0 ? N : 0;
+  return (d < ar) & (t >= at) & (t < at + aT);
+}
+
+template <typename R, int TW, bool SREC, int K>
+__global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
+  using C2 = typename cplx<R>::t;
+  using RecT = Rec<R>;
+  using MsgT = Msg<R, K>;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int C = P.C, lgC = ilog2(P.C);
+  const int rank = (int)cluster.block_rank();
+  const int W = P.W;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, NW = blockDim.x >> 5;
+  constexpr int LGTW = TW == 32 ? 5 : (TW == 64 ? 6 : 7);
+  constexpr int NCH = TW / 32;
+  const int NEc = min(NE, C * K);
+  const int B = max(1, min(BMAX, P.spec));
+
+  extern __shared__ __align__(32) unsigned char smem[];
+  const Smem L = smem_layout(P, sizeof(RecT), sizeof(MsgT));
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + L.mbar);
+  MsgT* mail = reinterpret_cast<MsgT*>(smem + L.mail);
+  MsgT* mymsg = reinterpret_cast<MsgT*>(smem + L.mymsg);
+  RecT* lev = reinterpret_cast<RecT*>(smem + L.lev);
+  Ent* ent = reinterpret_cast<Ent*>(smem + L.ent);
+  VGeo* egeo = reinterpret_cast<VGeo*>(smem + L.egeo);
+  uint32_t* wmeet = reinterpret_cast<uint32_t*>(smem + L.wmask);
+  uint32_t* wcover = wmeet + NE;
+  St* st = reinterpret_cast<St*>(smem + L.st);
+  uint32_t* vkey = reinterpret_cast<uint32_t*>(smem + L.vkey);
+  int* sorted = reinterpret_cast<int*>(smem + L.sorted);
+  int* tk = reinterpret_cast<int*>(smem + L.tk);
+  uint32_t* dirty = reinterpret_cast<uint32_t*>(smem + L.dirty);
+  PairGeo* sp = reinterpret_cast<PairGeo*>(smem + L.pairs);
+  DictGeo* sd = reinterpret_cast<DictGeo*>(smem + L.dicts);
+  OwnGeo* sown = reinterpret_cast<OwnGeo*>(smem + L.own);
+  const double2* roots = P.Rmax <= 4096 ? reinterpret_cast<const double2*>(smem + L.roots) : P.roots;
+  RhoEnt* srho = reinterpret_cast<RhoEnt*>(smem + L.rho);
+  int* rho_lo = reinterpret_cast<int*>(smem + L.rho_meta);
+  int* rho_n = rho_lo + W;
+  int* rho_off = rho_n + W;
+  RecT* grec = reinterpret_cast<RecT*>(P.rec) + (long long)rank * P.Lc;
+  RecT* trec = SREC ? reinterpret_cast<RecT*>(smem + L.trec) : grec;
+  C2* grid = reinterpret_cast<C2*>(P.grid);
+  const C2* kern = reinterpret_cast<const C2*>(P.kern);
+  C2* backup = reinterpret_cast<C2*>(P.backup) + (long long)rank * P.bk_cap * TW;
+  int* dw_off = reinterpret_cast<int*>(smem + L.dwoff);  // first dirty word of each level
+  if (tid == 0) {
+    dw_off[0] = 0;
+    for (int l = 0; l < MAX_LEVELS; ++l) dw_off[l + 1] = dw_off[l] + (l < P.nlev ? (P.lev_n[l] + 31) / 32 : 0);
+  }
+  __syncthreads();
+
+  // ---- load tables -------------------------------------------------------
+  for (int i = tid; i < W * W; i += blockDim.x) sp[i] = P.pairs[i];
+  for (int i = tid; i < W; i += blockDim.x) {
+    sd[i] = P.dicts[i];
+    sown[i] = P.own[rank * W + i];
+    rho_lo[i] = P.rho_lo[i];
+    rho_n[i] = P.rho_n[i];
+    rho_off[i] = P.rho_off[i];
+  }
+  if (P.Rmax <= 4096)
+    for (int i = tid; i < P.Rmax; i += blockDim.x) reinterpret_cast<double2*>(smem + L.roots)[i] = P.roots[i];
+  for (int i = tid; i < P.rho_total; i += blockDim.x) srho[i] = P.rho[i];
+  for (int i = tid; i < dw_off[P.nlev]; i += blockDim.x) dirty[i] = 0;
+  if (tid < BMAX) vkey[tid] = 0;
+  if (SREC)
+    for (long long i = tid; i < P.Lc; i += blockDim.x) trec[i] = grec[i];
+  __syncthreads();
+
+  // ---- node levels -------------------------------------------------------
+  for (int i = warp; i < P.lev_n[0]; i += NW) warp_node(trec, P.Lc, i, lev, lane);
+  __syncthreads();
+  for (int l = 1; l < P.nlev; ++l) {
+    for (int i = warp; i < P.lev_n[l]; i += NW)
+      warp_node(lev + P.lev_off[l - 1], (long long)P.lev_n[l - 1], i, lev + P.lev_off[l], lane);
+    __syncthreads();
+  }
+  const uint32_t msgbytes = (uint32_t)align_up(msg_head<R, K>() + sizeof(uint2) * K * W, 16);
+  if (tid == 0) {
+    mbar_init(smem_addr(&mbar[0]), 1);
+    mbar_init(smem_addr(&mbar[1]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_arm(smem_addr(&mbar[0]), C * msgbytes);
+    mbar_arm(smem_addr(&mbar[1]), C * msgbytes);
+    st->E = P.E0;
+    st->it = 0;
+    st->G = 0;
+    st->mode = 0;
+    st->rb_from = 0;
+    st->stop = 0;
+  }
+  cluster.sync();
+
+  const bool prof = P.prof != nullptr && rank == 0 && tid == 0;
+  long long tprev = clock64();
+#define PROF_MARK(i)                                                                                     \
+  if (prof) {                                                                                             \
+    const long long tn = clock64();                                                                      \
+    atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + (i), (unsigned long long)(tn - tprev)); \
+    tprev = tn;                                                                                           \
+  }
+
+  // warp 0: push the message (top-K records + per-candidate maxima) into slot
+  // `slot` of every CTA
+  auto publish = [&](int slot) {
+    if (lane < K) mymsg->list[lane] = tk[lane] >= 0 ? trec[tk[lane]] : empty_rec(R(0));
+    if (lane < BMAX) {
+      mymsg->vkey[lane] = vkey[lane];
+      vkey[lane] = 0;
+    }
+    // tiles(list[i]) in every target dictionary (CTA-independent part of Alg. 3's sets)
+    for (int t = lane; t < K * W; t += 32) {
+      const int i = t / W, v = t - i * W;
+      uint2 rc = make_uint2(0u, 0u);
+      if (tk[i] >= 0) {
+        const uint32_t p = trec[tk[i]].p;
+        int u, k, j;
+        decode_p(p, sd, W, u, k, j);
+        VGeo gg;
+        vgeo<LGTW>(sp[u * W + v], sd[u], sd[v], k, j, 0, C, lgC, gg);
+        rc = pack_rect(gg);
+      }
+      mymsg->rect[t] = rc;
+    }
+    __syncwarp();
+    PROF_MARK(13);
+    const int NCHUNK = (int)(msgbytes / 16);
+    const uint4* src = reinterpret_cast<const uint4*>(mymsg);
+    const uint32_t dst = smem_addr(&mail[slot * MAX_CLUSTER + rank]);
+    const uint32_t bar = smem_addr(&mbar[slot]);
+    for (int t = lane; t < C * NCHUNK; t += 32) {
+      const int d = t / NCHUNK, ch = t - d * NCHUNK;
+      st_async16(mapa(dst + 16 * ch, d), mapa(bar, d), src[ch]);
+    }
+    PROF_MARK(14);
+  };
+  cta_topk<R, K>(P, lev, trec, tk, lane, warp);
+  if (warp == 0) publish(0);
+
+  long long rounds = 0;
+  for (int round = 0;; ++round) {
+    const int par = round & 1;
+    const MsgT* mb = mail + par * MAX_CLUSTER;
+    // ---- A0/A1 (warp 0): messages of the previous round; verify its candidates
+    if (warp == 0) {
+      mbar_wait(smem_addr(&mbar[par]), (uint32_t)((round >> 1) & 1));
+      PROF_MARK(0);
+      if (lane == 0) mbar_arm(smem_addr(&mbar[par]), C * msgbytes);  // slot reused at round + 2
+      const int Gp = st->G;
+      int acc = Gp;
+      if (Gp >= 2) {
+        // V_l = max over CTAs of the candidate-l key; candidate i is accepted iff
+        // max_{l<i} V_l < key(c(p_i)) for it and every earlier candidate
+        uint4 va = make_uint4(0, 0, 0, 0), vb = make_uint4(0, 0, 0, 0);
+        if (lane < C) {
+          va = *reinterpret_cast<const uint4*>(&mb[lane].vkey[0]);
+          vb = *reinterpret_cast<const uint4*>(&mb[lane].vkey[4]);
+        }
+        const uint32_t vk[BMAX] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w};
+        uint32_t run = 0;
+#pragma unroll
+        for (int l = 0; l < BMAX - 1; ++l) {
+          const uint32_t V = __reduce_max_sync(0xffffffffu, vk[l]);
+          if (l < lane) run = max(run, V);
+        }
+        const bool fail = lane >= 1 && lane < Gp && run >= st->ckey[lane < BMAX ? lane : 0];
+        const unsigned fm = __ballot_sync(0xffffffffu, fail);
+        if (fm) acc = __ffs(fm) - 1;
+      }
+      if (lane == 0) {
+        if (acc > 0) {
+          if (rank == 0 && P.sol)  // c(p) += c~ for the accepted atoms, in order (Alg. 1 step 2a)
+            for (int g = 0; g < acc; ++g) {
+              const Ent& e = ent[g];
+              const DictGeo du = sd[e.u];
+              double2* s = P.sol + du.off + (long long)e.j * du.MR + e.k;
+              double2 c = *s;
+              c.x += e.tre;
+              c.y += e.tim;
+              *s = c;
+            }
+          st->it += acc;
+          st->E = st->Enext[acc - 1];
+        }
+        st->mode = acc < Gp ? 1 : 0;
+        st->rb_from = acc;
+      }
+      PROF_MARK(1);
+    }
+    __syncthreads();
+    if (warp != 0) mbar_wait(smem_addr(&mbar[par]), (uint32_t)((round >> 1) & 1));  // completed: acquire only
+    PROF_MARK(2);
+    const int mode = st->mode;
+    int lo = 0, hi = 0, gvend = 0;  // row-item range of this CTA, number of (g, v) pairs searched
+    if (mode == 0) {
+      // ---- A2: rank the C*K list entries: thread (e, c2) counts the entries of
+      //      list c2 ahead of e (score desc, index asc, then list order); 16 lanes sum
+      if (tid < NE) {
+        wmeet[tid] = 0;
+        wcover[tid] = 0;
+      }
+      const int CK = C * K;
+      for (int b0 = 0; b0 < CK * 16; b0 += blockDim.x) {
+        const int t = b0 + tid;
+        const int e = t >> 4, c2 = t & 15;
+        int rk = 0;
+        if (e < CK) {
+          const int c = e / K, i = e - c * K;
+          if (c2 == c) {
+            rk = i;
+          } else if (c2 < C) {
+            const uint64_t ks = skey64(mb[c].list[i].s);
+            const uint32_t p = mb[c].list[i].p;
+            const int cl = c2 < c;
+#pragma unroll
+            for (int i2 = 0; i2 < K; ++i2) {
+              const uint64_t ko = skey64(mb[c2].list[i2].s);
+              const uint32_t po = mb[c2].list[i2].p;
+              rk += (int)((ko > ks) | ((ko == ks) & ((po < p) | ((po == p) & cl))));
+            }
+          }
+        }
+#pragma unroll
+        for (int o = 8; o >= 1; o >>= 1) rk += __shfl_xor_sync(0xffffffffu, rk, o);
+        if (e < CK && c2 == 0 && rk < NEc) sorted[rk] = e;
+      }
+      PROF_MARK(3);
+      __syncthreads();
+      PROF_MARK(4);
+      // ---- A3: pairwise relations of the window entries (rects from the
+      //      publishers), one (a, v) pair per warp iteration, lane b:
+      //      meet[a] bit b  -- tiles(a) and tiles(b) share a tile of dictionary v
+      //      cover[a] bit b -- the tile of entry b lies in tiles(a)
+      {
+        int bu = -1, bj = 0, bt = 0, bsrc = 0;
+        if (lane < NEc) {
+          bsrc = sorted[lane];
+          const RecT& rb = mb[bsrc / K].list[bsrc % K];
+          if (rb.p != NO_INDEX) {
+            int bk;
+            decode_p(rb.p, sd, W, bu, bk, bj);
+            bt = bk >> LGTW;
+          }
+        }
+        const int bN = bu >= 0 ? sd[bu].N : 1;
+        for (int q = warp; q < NEc * W; q += NW) {
+          const int a = q / W, v = q - a * W;
+          const int asrc = sorted[a];
+          const uint2 ra = mb[asrc / K].rect[(asrc % K) * W + v];
+          bool meet = false, cover = false;
+          if (lane < NEc && ra.x != 0u) {
+            meet = rects_meet(ra, mb[bsrc / K].rect[(bsrc % K) * W + v], sd[v].N);
+            cover = bu == v && rect_has(ra, bj, bt, bN);
+          }
+          const unsigned mm = __ballot_sync(0xffffffffu, meet), cm = __ballot_sync(0xffffffffu, cover);
+          if (lane == 0 && (mm | cm)) {
+            if (mm) atomicOr(&wmeet[a], mm);
+            if (cm) atomicOr(&wcover[a], cm);
+          }
+        }
+      }
+      PROF_MARK(5);
+      __syncthreads();
+      PROF_MARK(6);
+      // ---- A4: the walk (warp 0, all lanes redundantly, bitmask logic) -----
+      if (warp == 0) {
+        const bool have = lane < NEc;
+        const int src = have ? sorted[lane] : 0;
+        const RecT rl = have ? mb[src / K].list[src % K] : empty_rec(R(0));
+        const unsigned lastm = __ballot_sync(0xffffffffu, have && (src % K) == K - 1);
+        const unsigned posm = __ballot_sync(0xffffffffu, have && rl.p != NO_INDEX && rl.s > R(0));
+        const unsigned win = NEc >= 32 ? 0xffffffffu : ((1u << NEc) - 1u);
+        const long long it0 = st->it;
+        const long long rem = P.maxit - it0;
+        const int Bm = rem < (long long)B ? (int)max(rem, 0LL) : B;
+        unsigned excl = 0, picked = 0, low = 0;
+        int G = 0;
+        int why = 0, lastpos = 0;  // walk statistics (profile mode)
+        while (true) {
+          if (G >= Bm) {
+            why = 1;
+            break;
+          }
+          const unsigned avail = win & ~excl & ~low;
+          if (!avail) {
+            why = 2;
+            break;
+          }
+          const int nx = __ffs(avail) - 1;
+          lastpos = nx;
+          const unsigned bit = 1u << nx;
+          if (lastm & excl & (bit - 1u) & ~low) {  // a CTA list ran out before nx
+            why = 3;
+            break;
+          }
+          if (!(posm & bit)) {  // zero score (stop rule 4 at G = 0)
+            why = 4;
+            break;
+          }
+          const unsigned mt = wmeet[nx], cv = wcover[nx];
+          if (mt & picked) {  // tiles(nx) meet X
+            why = 5;
+            break;
+          }
+          picked |= bit;
+          excl |= cv | bit;
+          ++G;
+          if (lastm & bit) {  // its CTA list is consumed
+            why = 6;
+            break;
+          }
+          low = (bit << 1) - 1u;
+        }
+        if (prof) {
+          atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 20, (unsigned long long)lastpos);
+          atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 20 + why, 1ull);
+        }
+        // candidate g = the g-th picked window entry: decode, scalar step (lane g)
+        if ((picked >> lane) & 1u) {
+          const int g = __popc(picked & ((1u << lane) - 1u));
+          Ent en;
+          decode_p(rl.p, sd, W, en.u, en.k, en.j);
+          en.key = score_key(rl.s);
+          const int u = en.u, k = en.k;
+          const int Mu = sd[u].M;
+          const bool selfc = (k == 0) || (2 * k == Mu);
+          en.selfc = selfc ? 1 : 0;
+          const double cre = (double)rl.re, cim = (double)rl.im;
+          if (selfc) {  // Z13
+            en.tre = cre;
+            en.tim = 0.0;
+            en.Et = cre * cre;
+          } else {      // Eqs. (19)-(20) with rho = h_uu(-2k, 0) (Z11/Z12)
+            int mu = (-2 * k) & (Mu - 1);
+            if (2 * mu > Mu) mu -= Mu;
+            double rre = 0.0, rim = 0.0, inv = 1.0;
+            const int ri = mu - rho_lo[u];
+            if (ri >= 0 && ri < rho_n[u]) {
+              const RhoEnt rv = srho[rho_off[u] + ri];
+              rre = rv.re;
+              rim = rv.im;
+              inv = rv.inv;
+            }
+            const double nre = cre - (rre * cre - rim * cim);
+            const double nim = cim + (rre * cim + rim * cre);
+            const double tre = nre * inv, tim = nim * inv;
+            const double X2 = tre * tre, Y2 = tim * tim, XY = tre * tim;
+            en.tre = tre;
+            en.tim = tim;
+            en.Et = 2.0 * (X2 + Y2 + rre * (X2 - Y2) - 2.0 * rim * XY);
+          }
+          ent[g] = en;
+        }
+        __syncwarp();
+        // update geometry of candidate g in dictionary v, seen from this CTA: lane
+        // handles the pairs (g, v) = lane + 32 s
+        for (int t = lane; t < G * W; t += 32) {
+          const int g = t / W, v = t - g * W;
+          const Ent& en = ent[g];
+          VGeo gg;
+          vgeo<LGTW>(sp[en.u * W + v], sd[en.u], sd[v], en.k, en.j, rank, C, lgC, gg);
+          egeo[t] = gg;
+        }
+        // E recurrence and the energy stop rules (Z15) in selection order
+        int Gs = 0, stopr = 0;
+        if (lane == 0) {
+          double Ecur = st->E;
+          for (; Gs < G; ++Gs) {
+            if (Ecur <= P.Etol || Ecur < 0.0) break;
+            const Ent& e = ent[Gs];
+            Ecur = Ecur - e.Et;
+            st->Enext[Gs] = Ecur;
+            st->ckey[Gs] = e.key;
+          }
+          if (Gs == 0) {
+            if (it0 >= P.maxit) stopr = 1;
+            else if (Ecur <= P.Etol) stopr = 2;
+            else if (Ecur < 0.0) stopr = 3;
+            else stopr = 4;
+          }
+          if (P.floor_mode && Gs > 1) Gs = 1;
+          st->G = Gs;
+          st->stop = stopr;
+        }
+        G = __shfl_sync(0xffffffffu, Gs, 0);
+        __syncwarp();
+        if (rank == 0 && lane < G) {  // atoms / energies (final once verified)
+          const Ent& e = ent[lane];
+          AtomOut a;
+          a.w = e.u;
+          a.m = e.k;
+          a.n = e.j;
+          a.flags = e.selfc;
+          a.re = e.tre;
+          a.im = e.tim;
+          P.atoms[it0 + lane] = a;
+          P.energy[it0 + lane + 1] = st->Enext[lane];
+        }
+        // this CTA's items (tile pairs of its rows) and tiles of (g, v), at index
+        // t = g * 16 + v (g-major; v >= W contribute nothing): lane handles 4 pairs
+        const int GW = G * 16;
+        int r4[4], t4[4], rs = 0, ts = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int t = lane * 4 + q;
+          int nrw = 0, ntl = 0;
+          const int g = t >> 4, v = t & 15;
+          if (t < GW && v < W && !P.floor_mode) {
+            const VGeo& gg = egeo[g * W + v];
+            const int rows = gg.nc > 0 ? gg.cntA + gg.cntB : 0;
+            nrw = rows * ((gg.Tr + 1) >> 1);
+            ntl = rows * gg.Tr;
+          }
+          r4[q] = nrw;
+          t4[q] = ntl;
+          rs += nrw;
+          ts += ntl;
+        }
+        int ri = rs, ti = ts;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y1 = __shfl_up_sync(0xffffffffu, ri, o), y2 = __shfl_up_sync(0xffffffffu, ti, o);
+          if (lane >= o) {
+            ri += y1;
+            ti += y2;
+          }
+        }
+        int rr = ri - rs, tt = ti - ts;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int t = lane * 4 + q;
+          if (t <= GW) {
+            st->ibase[t] = rr;
+            st->tbase[t] = tt;
+          }
+          rr += r4[q];
+          tt += t4[q];
+        }
+        if (lane == 31 && GW == 128) {
+          st->ibase[GW] = ri;
+          st->tbase[GW] = ti;
+        }
+      }
+      PROF_MARK(9);
+      __syncthreads();
+      PROF_MARK(10);
+      if (st->stop) {
+        ++rounds;
+        break;
+      }
+      lo = 0;
+      gvend = st->G * 16;
+      hi = st->ibase[gvend];
+    } else {
+      // roll back the rejected candidates' tiles (their items of the last round)
+      lo = st->ibase[st->rb_from * 16];
+      gvend = st->G * 16;
+      hi = st->ibase[gvend];
+      PROF_MARK(10);
+    }
+    ++rounds;
+    // ---- B. residual update (or roll-back) over this CTA's rows ------------
+    // tile bookkeeping: record, candidate maximum, dirty level-0 node (no returns)
+    auto finish = [&](int l, int g, R bs, uint32_t bp, R bre, R bim) {
+      R ws;
+      uint32_t wp;
+      const int wl = warp_argmax(bs, bp, ws, wp);
+      if (lane == wl) {
+        RecT rec;
+        rec.s = bs;
+        rec.re = bre;
+        rec.im = bim;
+        rec.p = bp;
+        if constexpr (sizeof(R) == 8) rec.pad = 0;
+        trec[l] = rec;
+        if (mode == 0) atomicMax(&vkey[g], score_key(bs));
+        const int node = l >> 5;
+        atomicOr(&dirty[node >> 5], 1u << (node & 31));
+      }
+    };
+    for (int gi = lo + warp; gi < hi; gi += NW) {
+      long long ta = prof ? clock64() : 0;
+      // (g, v) of item gi: count the item bases <= gi (ibase is non-decreasing)
+      int gv;
+      {
+        const int4 b4 = *reinterpret_cast<const int4*>(&st->ibase[lane * 4]);
+        const int i0 = lane * 4;
+        int c = 0;
+        c += (i0 + 0 >= 1 && i0 + 0 <= gvend && b4.x <= gi) ? 1 : 0;
+        c += (i0 + 1 >= 1 && i0 + 1 <= gvend && b4.y <= gi) ? 1 : 0;
+        c += (i0 + 2 <= gvend && b4.z <= gi) ? 1 : 0;
+        c += (i0 + 3 <= gvend && b4.w <= gi) ? 1 : 0;
+        gv = (int)__reduce_add_sync(0xffffffffu, (unsigned)c);
+      }
+      const int g = gv >> 4, v = gv & 15;
+      const VGeo& gg = egeo[g * W + v];
+      const DictGeo& dv = sd[v];
+      const int Tr = gg.Tr, t0 = gg.t0, MR = dv.MR;
+      const int hp = (Tr + 1) >> 1;
+      const int it = gi - st->ibase[gv];
+      const int i = it / hp;              // row among this CTA's rows of (g, v)
+      const int tt = 2 * (it - i * hp);   // first tile of the pair
+      const int r = i < gg.cntA ? gg.rhoA + (i << lgC) : gg.rA + gg.rhoB + ((i - gg.cntA) << lgC);
+      int nrow = gg.n0 + r;
+      if (nrow >= dv.N) nrow -= dv.N;
+      const int l0 = sown[v].loc_base + ((nrow - sown[v].n_first) >> lgC) * dv.T;
+      C2* row = grid + dv.grid_off + (long long)nrow * dv.stride;
+      C2* bkrow = backup + ((long long)st->tbase[gv] + (long long)i * Tr) * TW;
+      const uint32_t pbase = (uint32_t)dv.off + (uint32_t)nrow * (uint32_t)MR;
+      if (mode == 1) {
+        for (int q = 0; q < 2 && tt + q < Tr; ++q) {
+          const int t = t0 + tt + q;
+          const C2* bk = bkrow + (long long)(tt + q) * TW;
+          C2 cv[NCH];
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch) {
+            const int bin = t * TW + ch * 32 + lane;
+            if (bin < MR) cv[ch] = bk[ch * 32 + lane];
+          }
+          R bs = 0, bre = 0, bim = 0;
+          uint32_t bp = NO_INDEX;
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch) {
+            const int bin = t * TW + ch * 32 + lane;
+            if (bin < MR) {
+              const C2 c = cv[ch];
+              row[bin] = c;
+              const R s = ScoreOps<R>::score(c.x, c.y);
+              const uint32_t p = pbase + (uint32_t)bin;
+              if (better(s, p, bs, bp)) {
+                bs = s;
+                bp = p;
+                bre = c.x;
+                bim = c.y;
+              }
+            }
+          }
+          finish(l0 + t, g, bs, bp, bre, bim);
+        }
+      } else {
+        const Ent& en = ent[g];
+        const PairGeo& pg = sp[en.u * W + v];
+        const bool selfc = en.selfc != 0;
+        // modulation omega_R^{(k' nu) mod R} of this row (Eq. (15))
+        const int rrx = (gg.rr0 + r * gg.rrstep) & (pg.R - 1);
+        const double2 w = roots[rrx * pg.rstep];
+        const C2 z0 = row_z0<C2, R>(en.tre, en.tim, w);
+        const C2* hrow = kern + gg.kbase + (long long)r * gg.nc;
+        const int q0 = gg.q0, nc = gg.nc, Mv = dv.M;
+        if (prof) {
+          const long long tn = clock64();
+          atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 16, (unsigned long long)(tn - ta));
+          atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 19, 1ull);
+          ta = tn;
+        }
+        C2 cv[2][NCH], hd[2][NCH], hc[2][NCH];
+        bool fd[2][NCH], fc[2][NCH], cf[2][NCH];
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch) {  // issue every load before any store
+            const int bin = (t0 + tt + q) * TW + ch * 32 + lane;
+            const bool valid = (tt + q < Tr) && bin < MR;
+            const int cd = (bin - q0) & (Mv - 1);   // direct source column  (q = bin)
+            const int cc = (-bin - q0) & (Mv - 1);  // conjugate source column (q = M - bin)
+            fd[q][ch] = valid && cd < nc;
+            fc[q][ch] = valid && !selfc && cc < nc;
+            cf[q][ch] = cc < cd;                    // oracle order: ascending source column
+            cv[q][ch] = valid ? row[bin] : C2{0, 0};
+            hd[q][ch] = fd[q][ch] ? hrow[cd] : C2{0, 0};
+            hc[q][ch] = fc[q][ch] ? hrow[cc] : C2{0, 0};
+          }
+        if (g > 0) {  // speculative candidate: keep the tiles for a roll-back
+#pragma unroll
+          for (int q = 0; q < 2; ++q)
+#pragma unroll
+            for (int ch = 0; ch < NCH; ++ch)
+              if (tt + q < Tr && (t0 + tt + q) * TW + ch * 32 + lane < MR)
+                bkrow[(long long)(tt + q) * TW + ch * 32 + lane] = cv[q][ch];
+        }
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          if (tt + q >= Tr) break;
+          const int t = t0 + tt + q;
+          R bs = 0, bre = 0, bim = 0;
+          uint32_t bp = NO_INDEX;
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch) {
+            const int bin = t * TW + ch * 32 + lane;
+            if (prof && ch == 0 && q == 0) {  // first use of the loaded tile
+              const long long tn = clock64();
+              atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 17, (unsigned long long)(tn - ta));
+              ta = tn;
+            }
+            const C2 c = fold_update<R>(cv[q][ch], z0, hd[q][ch], hc[q][ch], fd[q][ch], fc[q][ch], cf[q][ch]);
+            if (bin < MR) {
+              if (fd[q][ch] || fc[q][ch]) row[bin] = c;
+              const R s = ScoreOps<R>::score(c.x, c.y);
+              const uint32_t p = pbase + (uint32_t)bin;
+              if (better(s, p, bs, bp)) {
+                bs = s;
+                bp = p;
+                bre = c.x;
+                bim = c.y;
+              }
+            }
+          }
+          finish(l0 + t, g, bs, bp, bre, bim);
+        }
+        if (prof) {
+          const long long tn = clock64();
+          atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 18, (unsigned long long)(tn - ta));
+        }
+      }
+    }
+    PROF_MARK(11);
+    __syncthreads();
+    // ---- C. level-0 refresh of the dirty nodes (set bits of the level-0 words)
+    {
+      const int nw = dw_off[1];
+      // every warp enumerates the same set bits; the r-th goes to warp r mod NW
+      int base = 0;
+      for (int w0 = 0; w0 < nw; w0 += 32) {
+        const uint32_t word = w0 + lane < nw ? dirty[w0 + lane] : 0u;
+        const int cntw = __popc(word);
+        int incl = cntw;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        const int first = (warp - base % NW + NW) % NW;  // first rank of this warp in this chunk
+        for (int rr = first; rr < total; rr += NW) {
+          const unsigned hold = __ballot_sync(0xffffffffu, incl > rr && incl - cntw <= rr);
+          const int src = __ffs(hold) - 1;
+          uint32_t wd = __shfl_sync(0xffffffffu, word, src);
+          const int k = rr - __shfl_sync(0xffffffffu, incl - cntw, src);
+          for (int q = 0; q < k; ++q) wd &= wd - 1u;  // drop the k lower set bits
+          const int node = (w0 + src) * 32 + __ffs(wd) - 1;
+          const long long c = (long long)node * 32 + lane;
+          const RecT rc = c < P.Lc ? trec[c] : empty_rec(R(0));
+          R s;
+          uint32_t p;
+          const int wl = warp_argmax(rc.s, rc.p, s, p);
+          if (lane == wl) {
+            lev[node] = rc;
+            if (P.nlev > 1) atomicOr(&dirty[dw_off[1] + (node >> 10)], 1u << ((node >> 5) & 31));
+          }
+        }
+        base += total;
+      }
+    }
+    __syncthreads();
+    PROF_MARK(12);
+    // ---- D. upper levels, top-K, publish (warp 0) ---------------------------
+    if (warp == 0) {
+      for (int l = 1; l < P.nlev; ++l) {
+        for (int w0 = dw_off[l]; w0 < dw_off[l + 1]; ++w0) {
+          uint32_t word = dirty[w0];
+          while (word) {
+            const int b = __ffs(word) - 1;
+            word &= word - 1u;
+            const int node = (w0 - dw_off[l]) * 32 + b;
+            const int c = node * 32 + lane;
+            const RecT rc = c < P.lev_n[l - 1] ? lev[P.lev_off[l - 1] + c] : empty_rec(R(0));
+            R s;
+            uint32_t p;
+            const int wl = warp_argmax(rc.s, rc.p, s, p);
+            if (lane == wl) {
+              lev[P.lev_off[l] + node] = rc;
+              if (l + 1 < P.nlev) atomicOr(&dirty[dw_off[l + 1] + (node >> 10)], 1u << ((node >> 5) & 31));
+            }
+            __syncwarp();
+          }
+        }
+      }
+      for (int i = lane; i < dw_off[P.nlev]; i += 32) dirty[i] = 0;
+      if (lane == 0 && mode == 1) st->G = 0;  // nothing to verify after a roll-back
+    }
+    __syncthreads();
+    cta_topk<R, K>(P, lev, trec, tk, lane, warp);
+    if (warp == 0) publish(par ^ 1);
+  }
+  if (rank == 0 && tid == 0) {
+    P.result->n_done = st->it;
+    P.result->stop = st->stop;
+    P.result->E_final = st->E;
+    P.result->rounds = rounds;
+  }
+  if (prof) P.prof[15] = rounds;
+#undef PROF_MARK
+  cluster.sync();  // keep every CTA's shared memory alive until all remote stores are done
+}
+
+template <typename R, int TW, bool SREC, int K>
+cudaError_t launch_t(const LoopParams& P, int threads, cudaStream_t st) {
+  auto kfn = mp_multi_kernel<R, TW, SREC, K>;
+  CUDA_OK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem_bytes));
+  if (P.C > 8) CUDA_OK(cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(P.C, 1, 1);
+  cfg.blockDim = dim3(threads, 1, 1);
+  cfg.dynamicSmemBytes = P.smem_bytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = P.C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kfn, P);
+}
+
+template <typename R, int TW, bool SREC, int K>
+int max_cluster_t(int threads, size_t smem) {
+  auto kfn = mp_multi_kernel<R, TW, SREC, K>;
+  if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+      cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  for (int c = MAX_CLUSTER; c >= 1; c >>= 1) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(c, 1, 1);
+    cfg.blockDim = dim3(threads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = c;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kfn, &cfg) == cudaSuccess && n > 0) return c;
+    cudaGetLastError();
+  }
+  return 0;
+}
+
+template <typename R, bool SREC>
+cudaError_t launch_r(const LoopParams& P, int threads, cudaStream_t st) {
+  switch (P.TW) {
+    case 32: return launch_t<R, 32, SREC, MULTI_K>(P, threads, st);
+    case 64: return launch_t<R, 64, SREC, MULTI_K>(P, threads, st);
+    case 128: return launch_t<R, 128, SREC, MULTI_K>(P, threads, st);
+  }
+  return cudaErrorInvalidValue;
+}
+template <typename R, bool SREC>
+int max_cluster_r(int TW, int threads, size_t smem) {
+  switch (TW) {
+    case 32: return max_cluster_t<R, 32, SREC, MULTI_K>(threads, smem);
+    case 64: return max_cluster_t<R, 64, SREC, MULTI_K>(threads, smem);
+    case 128: return max_cluster_t<R, 128, SREC, MULTI_K>(threads, smem);
+  }
+  return 0;
+}
+
+}  // namespace
+
+size_t multi_smem_bytes(const LoopParams& P, bool f64) {
+  return f64 ? smem_layout(P, sizeof(Rec<double>), sizeof(Msg<double, MULTI_K>)).total
+             : smem_layout(P, sizeof(Rec<float>), sizeof(Msg<float, MULTI_K>)).total;
+}
+
+int multi_max_batch() { return BMAX; }
+
+cudaError_t launch_multi_loop(const LoopParams& P, bool f64, int threads, cudaStream_t st) {
+  if (f64) return P.srec ? launch_r<double, true>(P, threads, st) : launch_r<double, false>(P, threads, st);
+  return P.srec ? launch_r<float, true>(P, threads, st) : launch_r<float, false>(P, threads, st);
+}
+
+int multi_max_cluster(bool f64, bool srec, int TW, int threads, size_t smem) {
+  if (f64) return srec ? max_cluster_r<double, true>(TW, threads, smem) : max_cluster_r<double, false>(TW, threads, smem);
+  return srec ? max_cluster_r<float, true>(TW, threads, smem) : max_cluster_r<float, false>(TW, threads, smem);
+}

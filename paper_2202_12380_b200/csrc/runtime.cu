@@ -93,7 +93,7 @@ struct mpgabor {
   long long trace_it0 = 0;
   int trace_n = 0;
   DevBuf trace;
-  long long prof_host[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long prof_host[32] = {};
   DevBuf prof;
   cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   float t_dgt = 0, t_init = 0, t_loop = 0;
@@ -708,8 +708,8 @@ extern "C" int mpgabor_run(mpgabor* h, const double* x_dev, int64_t Ls, int64_t 
   }
   P.prof = nullptr;
   if (h->prof_mode & 1) {
-    TRY_CUDA(h, h->prof.ensure(sizeof(long long) * 8));
-    TRY_CUDA(h, cudaMemsetAsync(h->prof.p, 0, sizeof(long long) * 8, st));
+    TRY_CUDA(h, h->prof.ensure(sizeof(long long) * 32));
+    TRY_CUDA(h, cudaMemsetAsync(h->prof.p, 0, sizeof(long long) * 32, st));
     P.prof = h->prof.as<long long>();
   }
   TRY_CUDA(h, cudaEventRecord(h->ev[3], st));
@@ -727,7 +727,7 @@ extern "C" int mpgabor_run(mpgabor* h, const double* x_dev, int64_t Ls, int64_t 
   TRY_CUDA(h, cudaEventElapsedTime(&h->t_dgt, h->ev[0], h->ev[1]));
   TRY_CUDA(h, cudaEventElapsedTime(&h->t_init, h->ev[1], h->ev[2]));
   TRY_CUDA(h, cudaEventElapsedTime(&h->t_loop, h->ev[3], h->ev[4]));
-  if (P.prof) TRY_CUDA(h, cudaMemcpy(h->prof_host, P.prof, sizeof(long long) * 8, cudaMemcpyDeviceToHost));
+  if (P.prof) TRY_CUDA(h, cudaMemcpy(h->prof_host, P.prof, sizeof(long long) * 32, cudaMemcpyDeviceToHost));
   res->n_atoms = lr.n_done;
   res->L_pad = h->L;
   res->stop_reason = lr.stop;
@@ -795,7 +795,7 @@ extern "C" int mpgabor_set_profile(mpgabor* h, int32_t mode) {
 
 extern "C" int mpgabor_last_profile(const mpgabor* h, int64_t* cycles) {
   if (!h || !cycles) return MPG_EINVAL;
-  for (int i = 0; i < 8; ++i) cycles[i] = h->prof_host[i];
+  for (int i = 0; i < 32; ++i) cycles[i] = h->prof_host[i];
   return MPG_OK;
 }
 

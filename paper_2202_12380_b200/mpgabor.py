@@ -221,7 +221,7 @@ def mpgabor_set_profile(h, mode):
 
 
 def mpgabor_last_profile(h):
-    c = (_I64 * 8)()
+    c = (_I64 * 32)()
     _check(h, _lib.mpgabor_last_profile(h, c))
     return list(c)
 

@@ -1,0 +1,41 @@
+"""Dev tool: per-phase time per round of the multi-selection loop (profile mode bit 0).
+
+Slots (mpgabor.h, mpgabor_last_profile): 0 wait, 1 verify, 2 bar, 3 rank, 4 bar, 5 geometry,
+6 bar, 7 pairwise, 8 bar, 9 walk, 10 bar, 11 own items, 12 bar+lvl1+bar, 13 top-K, 14 push; 15 rounds.
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+import siggen
+from paper_2202_12380_b200.mpgabor import MPGabor
+
+PH = ["wait", "verify", "b", "rank", "b", "pair", "b", "-", "-", "walk", "b", "items", "lvl1", "topk", "push"]
+cfgs = sys.argv[1].split(",") if len(sys.argv) > 1 else ["C2"]
+K = int(sys.argv[2]) if len(sys.argv) > 2 else 100000
+batches = [int(b) for b in sys.argv[3].split(",")] if len(sys.argv) > 3 else [8]
+prec = sys.argv[4] if len(sys.argv) > 4 else "f64"
+for name in cfgs:
+    cfg = siggen.CONFIGS[name]
+    xd = torch.from_numpy(siggen.signal(cfg)).cuda()
+    mp = MPGabor(cfg.dicts, cfg.thr, prec)
+    for b in batches:
+        mp.set_batch(b)
+        mp.set_profile(1)
+        mp.run(xd, K, cfg.errdb, fetch=False)
+        res, _ = mp.run(xd, K, cfg.errdb, fetch=False)
+        c = mp.last_profile()
+        loop = mp.last_timing()[2]
+        n = max(1, c[15] if b != 1 else c[7])
+        print(f"{name} {prec} batch={b}: atoms {res.n_atoms} rounds {n} loop {loop:.2f} ms "
+              f"({1e3 * loop / n:.3f} us/round, {1e3 * loop / max(res.n_atoms, 1):.3f} us/atom) | "
+              + " ".join(f"{p}={x / n:.0f}" for p, x in zip(PH, c[:15])) + " cycles/round", flush=True)
+        print(f"   walk: mean last window position {c[20] / n:.1f}; ends: B {c[21]} window {c[22]} "
+              f"list-exhausted {c[23]} zero/stop {c[24]} overlap {c[25]} last-entry {c[26]}", flush=True)
+        if c[19]:
+            print(f"   thread-0 items: {c[19]} ({c[19] / n:.2f}/round) setup {c[16] / c[19]:.0f} loads {c[17] / c[19]:.0f} "
+                  f"update+bookkeeping {c[18] / c[19]:.0f} cycles/item", flush=True)
+        mp.set_profile(0)
+    mp.close()
