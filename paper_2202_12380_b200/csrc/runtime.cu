@@ -75,6 +75,7 @@ struct mpgabor {
   int run_threads = 512;  // threads of the planned loop launch
   int batch = 0;          // candidates per round: 0 auto (multi-selection, multi_max_batch()), 1 one selection
   int kind = 2;           // loop kernel: 0 mploop.cu, 1 mplean.cu, 2 mpmulti.cu
+  bool force_single = false;  // multi-selection impossible for this layout: use mploop.cu
 
   // per-length layout
   int64_t L = -1, Ls_cached = -1;
@@ -516,7 +517,7 @@ static size_t plan_loop(mpgabor* h, int TW, int srec, int C) {
   }
   P.nlev = nl;
   // loop kernel: 2 = mpmulti.cu (default), 0 = mploop.cu (batch 1), 1 = mplean.cu (profile-mode bit 2)
-  const int kind = (h->prof_mode & 4) ? 1 : (h->batch == 1 ? 0 : 2);
+  const int kind = (h->prof_mode & 4) ? 1 : ((h->batch == 1 || h->force_single) ? 0 : 2);
   h->kind = kind;
   h->run_threads = h->threads;
   P.spec = h->batch == 0 ? multi_max_batch() : h->batch;
@@ -552,6 +553,18 @@ static int ensure_layout(mpgabor* h, int64_t Ls) {
   if (h->srec_req != 1) cands.push_back({tws[0], 0});
   std::string why = "no candidate";
   bool ok = false;
+  // the multi-selection kernel packs tile rects as (row 20 bits, rows 12 bits) and
+  // needs more shared memory: fall back to the one-selection kernel when it cannot run
+  h->force_single = false;
+  for (int v = 0; v < W; ++v)
+    if (L / h->dicts[v].a >= (1 << 20)) h->force_single = true;
+  for (int i = 0; i < W * W; ++i)
+    if ((h->pairs[i].nnu + h->pairs[i].s_n - 1) / h->pairs[i].s_n >= (1 << 12)) h->force_single = true;
+  for (int attempt = 0; attempt < 2 && !ok; ++attempt) {
+  if (attempt == 1) {
+    if (h->kind != 2) break;
+    h->force_single = true;
+  }
   for (const Cand& c : cands) {
     int rc = plan_grids(h, L, c.TW);
     if (rc) return rc;
@@ -576,6 +589,7 @@ static int ensure_layout(mpgabor* h, int64_t Ls) {
       h->srec = c.srec;
       break;
     }
+  }
   }
   if (!ok) return h->fail(MPG_ECUDA, "no launch plan for the MP loop: " + why);
   LoopParams& P = h->lp;

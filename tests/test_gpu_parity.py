@@ -56,10 +56,12 @@ def ref_of(name, K):
     return _REFS[key]
 
 
-def gpu_run(mpg, dicts, thr, x, K, errdb, prec="f64", launch=None, want_coef=False):
+def gpu_run(mpg, dicts, thr, x, K, errdb, prec="f64", launch=None, want_coef=False, batch=None):
     mp = mpg.MPGabor(dicts, thr, prec)
     if launch:
         mp.set_launch(*launch)
+    if batch is not None:
+        mp.set_batch(batch)
     out = mp.run(torch.from_numpy(np.ascontiguousarray(x)).cuda(), K, errdb, want_coef=want_coef)
     lay = mp.layout(x.size)
     return mp, out, out.index(lay[3], lay[2])
@@ -127,12 +129,13 @@ def test_dgt_matches_oracle(mpg, name, prec):
 # ---------------------------------------------------------------------------
 # full runs
 # ---------------------------------------------------------------------------
+@pytest.mark.parametrize("batch", [1, 0])   # one selection per iteration; exact multi-selection
 @pytest.mark.parametrize("name", ["C0", "C1", "C2"])
-def test_full_run_fp64(mpg, name):
+def test_full_run_fp64(mpg, name, batch):
     cfg = CONFIGS[name]
     x, S = setup_of(name)
     ref = ref_of(name, cfg.maxit)
-    mp, out, idx = gpu_run(mpg, cfg.dicts, cfg.thr, x, cfg.maxit, cfg.errdb, "f64", want_coef=True)
+    mp, out, idx = gpu_run(mpg, cfg.dicts, cfg.thr, x, cfg.maxit, cfg.errdb, "f64", want_coef=True, batch=batch)
     assert_fp64_parity(out, idx, ref)
     np.testing.assert_allclose(out.atoms["re"], ref.atoms["re"], rtol=0, atol=1e-9 * math.sqrt(S.E0))
     np.testing.assert_allclose(out.atoms["im"], ref.atoms["im"], rtol=0, atol=1e-9 * math.sqrt(S.E0))
@@ -162,13 +165,14 @@ def test_full_run_fp32(mpg, name):
 PREFIX = {"C3": 20000, "C4": 4000}
 
 
+@pytest.mark.parametrize("batch", [1, 0])
 @pytest.mark.parametrize("name,prec", [("C3", "f64"), ("C4", "f64"), ("C3", "f32"), ("C4", "f32")])
-def test_prefix_parity_large(mpg, name, prec):
+def test_prefix_parity_large(mpg, name, prec, batch):
     cfg = CONFIGS[name]
     x, S = setup_of(name)
     K = PREFIX[name]
     ref = ref_of(name, K)
-    mp, out, idx = gpu_run(mpg, cfg.dicts, cfg.thr, x, K, cfg.errdb, prec)
+    mp, out, idx = gpu_run(mpg, cfg.dicts, cfg.thr, x, K, cfg.errdb, prec, batch=batch)
     if prec == "f64":
         assert_fp64_parity(out, idx, ref)
     else:
@@ -219,15 +223,60 @@ def test_full_length_sampled(mpg, name, prec):
 
 
 # ---------------------------------------------------------------------------
-# launch configurations, determinism, host API
+# exact multi-selection: every batch gives the bitwise
+# identical decomposition of the one-selection loop, roll-backs included
 # ---------------------------------------------------------------------------
-@pytest.mark.parametrize("launch", [(1, 512, 64, 0), (2, 128, 32, 1), (4, 256, 128, 1), (8, 512, 64, 2),
-                                    (16, 256, 32, 2), (16, 512, 128, 1)])
-def test_launch_configurations_identical(mpg, launch):
+MULTI_CASES = [("C0", "f64", 500), ("C1", "f64", 4000), ("C2", "f64", 6000), ("C2", "f32", 6000),
+               ("C3", "f64", 3000), ("C4", "f64", 1500), ("C4", "f32", 1500)]
+
+
+@pytest.mark.parametrize("name,prec,K", MULTI_CASES)
+def test_multi_selection_bitwise_identical(mpg, name, prec, K):
+    cfg = CONFIGS[name]
+    x, S = setup_of(name)
+    xd = torch.from_numpy(x).cuda()
+    mp = mpg.MPGabor(cfg.dicts, cfg.thr, prec)
+    mp.set_batch(1)
+    ref = mp.run(xd, K, cfg.errdb)
+    res_ref = mp.residual(cfg.Ls).cpu().numpy()
+    assert ref.rounds == ref.n + 1
+    for b in (2, 5, 8):
+        mp.set_batch(b)
+        out = mp.run(xd, K, cfg.errdb)
+        assert out.n == ref.n and out.stop == ref.stop
+        assert out.atoms.tobytes() == ref.atoms.tobytes(), f"batch {b}"
+        assert out.energy.tobytes() == ref.energy.tobytes(), f"batch {b}"
+        assert np.array_equal(mp.residual(cfg.Ls).cpu().numpy(), res_ref), f"batch {b}"
+        # several atoms per round on average, and rounds are bounded by the batch
+        assert ref.n / b <= out.rounds <= ref.n + 1
+        if b == 8 and ref.n >= 1000:
+            assert out.rounds < 0.6 * ref.n, (out.rounds, ref.n)
+    mp.close()
+
+
+def test_multi_selection_solution_vector(mpg):
+    # the solution vector c (Alg. 1 step 2a) only accumulates verified atoms
     cfg = CONFIGS["C1"]
     x, S = setup_of("C1")
     ref = ref_of("C1", 3000)
-    mp, out, idx = gpu_run(mpg, cfg.dicts, cfg.thr, x, 3000, cfg.errdb, "f64", launch=launch)
+    mp, out, idx = gpu_run(mpg, cfg.dicts, cfg.thr, x, 3000, cfg.errdb, "f64", want_coef=True, batch=8)
+    assert_fp64_parity(out, idx, ref)
+    coef = out.coef.cpu().numpy()
+    assert np.max(np.abs(coef - ref.sol)) <= 1e-9 * math.sqrt(S.E0)
+    mp.close()
+
+
+# ---------------------------------------------------------------------------
+# launch configurations, determinism, host API
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("batch", [1, 0])
+@pytest.mark.parametrize("launch", [(1, 512, 64, 0), (2, 128, 32, 1), (4, 256, 128, 1), (8, 512, 64, 2),
+                                    (16, 256, 32, 2), (16, 512, 128, 1)])
+def test_launch_configurations_identical(mpg, launch, batch):
+    cfg = CONFIGS["C1"]
+    x, S = setup_of("C1")
+    ref = ref_of("C1", 3000)
+    mp, out, idx = gpu_run(mpg, cfg.dicts, cfg.thr, x, 3000, cfg.errdb, "f64", launch=launch, batch=batch)
     info = mp.launch_info()
     assert info["cluster"] == launch[0] and info["tile_width"] == launch[2]
     assert_fp64_parity(out, idx, ref)
@@ -306,14 +355,15 @@ TINY = [
 ]
 
 
+@pytest.mark.parametrize("batch", [1, 0])
 @pytest.mark.parametrize("dicts,Ls", TINY)
 @pytest.mark.parametrize("thr", [0.0, 1e-4, 1e-2])
-def test_tiny_dictionaries(mpg, dicts, Ls, thr):
+def test_tiny_dictionaries(mpg, dicts, Ls, thr, batch):
     # stop at -60 dB so that E_k stays far from 0 (its relative error is ill-conditioned there)
     x = random_signal(Ls, 11)
     S = oracle.Setup.build(x, dicts, thr)
     ref = oloop.mp_run(S, 150, -60.0)
-    mp, out, idx = gpu_run(mpg, dicts, thr, x, 150, -60.0, "f64")
+    mp, out, idx = gpu_run(mpg, dicts, thr, x, 150, -60.0, "f64", batch=batch)
     assert_fp64_parity(out, idx, ref)
     if thr == 0.0:   # eps = 0: equals exact signal-domain MP (Eq. (8))
         at, e, te, _, _ = dense.signal_mp(x, dicts, 150, -60.0)
