@@ -161,9 +161,12 @@ int mpgabor_set_launch(mpgabor* h, int32_t cluster, int32_t threads, int32_t til
  * atoms are verified against the sequential argmax rule (Alg. 1, ties
  * Z10) and rolled back bit-exactly when the proof fails, so the atom sequence,
  * coefficients and energies are those of the one-selection loop for every value.
- * 0 = automatic (the largest batch, 8), 1 = one selection per iteration (the
- * plain persistent loop), 2..8 = that batch.  EINVAL outside [0, 8].  Takes
- * effect at the next run. */
+ * 0 = automatic: batch 8 when the mean update of an atom is small (< 1500
+ * coefficients, estimated from the kernel boxes, and < 0.5 % of the reduced
+ * coefficients), else one selection per
+ * iteration (DESIGN.md §8 has the measured crossover); 1 = one selection per
+ * iteration (the plain persistent loop); 2..8 = that batch.  EINVAL outside
+ * [0, 8].  Takes effect at the next run. */
 int mpgabor_set_batch(mpgabor* h, int32_t max_batch);
 /* The launch plan used by the last mpgabor_run (host outputs, may be NULL);
  * records: 1 shared memory, 2 global memory. */

@@ -49,7 +49,7 @@ namespace {
 
 using namespace mpcore;
 
-constexpr int NE = 16;    // walk window: best merged list entries considered per round
+constexpr int NE = 8;     // walk window: best merged list entries considered per round
 constexpr int BMAX = 8;   // candidates per round (upper bound; LoopParams::spec lowers it)
 
 template <typename R, int K>

@@ -478,6 +478,28 @@ static int plan_grids(mpgabor* h, int64_t L, int TW) {
   return MPG_OK;
 }
 
+// Automatic choice between the loop kernels (mpgabor_set_batch 0).  A multi-selection
+// round has a fixed cost of ~20k SM cycles (list exchange, ranking, walk, top-K) and
+// yields ~5 atoms; an iteration of the one-selection loop costs ~5k cycles plus its
+// share of the update.  Measured on B200: multi-selection wins while
+// an atom's update is small (C1: 675 coefficients, 2.1 vs 2.6 us/atom), breaks even
+// near C2 (2,176) and loses on C3/C4 (18.5k / 56k).  Estimate the mean update size
+// from the kernel boxes (subsampled per target, averaged over the selected dictionary)
+// and require it to be a small fraction of the grid.
+static bool auto_multi(const mpgabor* h) {
+  const int W = h->W;
+  double sum = 0.0;
+  for (int u = 0; u < W; ++u)
+    for (int v = 0; v < W; ++v) {
+      const PairGeo& pg = h->pairs[u * W + v];
+      sum += (double)pg.nnu / pg.s_n * ((double)pg.nmu / pg.s_m);
+    }
+  const double per_atom = sum / W;
+  // rounds need independent atoms: small patches relative to the grid (C0's patch
+  // covers 2.6 % of its grid and gives ~2 atoms per round)
+  return per_atom < 1500.0 && per_atom < 0.005 * (double)h->P_R;
+}
+
 // loop parameters for (TW, srec, C); returns shared-memory bytes (SIZE_MAX if the tree is too deep)
 static size_t plan_loop(mpgabor* h, int TW, int srec, int C) {
   LoopParams& P = h->lp;
@@ -517,7 +539,7 @@ static size_t plan_loop(mpgabor* h, int TW, int srec, int C) {
   }
   P.nlev = nl;
   // loop kernel: 2 = mpmulti.cu (default), 0 = mploop.cu (batch 1), 1 = mplean.cu (profile-mode bit 2)
-  const int kind = (h->prof_mode & 4) ? 1 : ((h->batch == 1 || h->force_single) ? 0 : 2);
+  const int kind = (h->prof_mode & 4) ? 1 : ((h->batch == 1 || h->force_single || (h->batch == 0 && !auto_multi(h))) ? 0 : 2);
   h->kind = kind;
   h->run_threads = h->threads;
   P.spec = h->batch == 0 ? multi_max_batch() : h->batch;
