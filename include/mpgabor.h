@@ -203,7 +203,8 @@ int mpgabor_residual(mpgabor* h, double* out_dev, void* cuda_stream);
  * mode bit0 = accumulate per-phase SM clock cycles on CTA 0 / thread 0;
  * mode bit1 = latency-floor mode: the residual update is skipped (selection,
  * scalar step, max refresh and the cluster barrier still run) -- the results
- * of such a run are NOT a decomposition and must only be used for timing. */
+ * of such a run are NOT a decomposition and must only be used for timing
+ * (one-selection kernel).  EINVAL outside [0, 3]. */
 int mpgabor_set_profile(mpgabor* h, int32_t mode);
 
 /* cycles (host int64[32]) of the last run with mode bit0, summed over the
@@ -219,15 +220,6 @@ int mpgabor_set_profile(mpgabor* h, int32_t mode);
  * [14] message push; [15] rounds; [16..19] own items: set-up, loads and
  * update, tile bookkeeping, items processed. */
 int mpgabor_last_profile(const mpgabor* h, int64_t* cycles);
-
-/* Event timeline of iterations [it0, it0+n) of the next runs (n = 0 disables):
- * per iteration and CTA, `slots` int64 values (globaltimer ns unless noted):
- * [0] roots received, [1] selection + scalar done, [2] geometry done, [3] after
- * the block barrier, [4] root published, [5] items of the CTA (count), [6] dirty
- * level-1 nodes (count), [7] clean-part max done, [8 + w] warp w finished its items. */
-int mpgabor_set_trace(mpgabor* h, int64_t it0, int32_t n);
-/* Copy the timeline (host int64[n * ctas * slots], row-major [it][cta][slot]). */
-int mpgabor_last_trace(mpgabor* h, int64_t* host, int64_t cap, int32_t* slots, int32_t* ctas);
 
 void mpgabor_destroy(mpgabor* h);
 

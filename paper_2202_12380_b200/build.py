@@ -4,7 +4,7 @@ import subprocess
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libmpgabor.so")
-SOURCES = ["csrc/analysis.cu", "csrc/mplean.cu", "csrc/mploop.cu", "csrc/mpmulti.cu", "csrc/synth.cu", "csrc/runtime.cu"]
+SOURCES = ["csrc/analysis.cu", "csrc/mploop.cu", "csrc/mpmulti.cu", "csrc/synth.cu", "csrc/runtime.cu"]
 HEADERS = ["csrc/common.cuh", "csrc/fft.cuh", "csrc/launch.h", "csrc/loopcore.cuh", "csrc/argmax.cuh", "../include/mpgabor.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -70,9 +70,6 @@ struct LoopParams {
   LoopResult* result;
   long long* prof;               // optional [8] clock64 phase sums (rank 0, thread 0), [7] = iterations
   int floor_mode;                // 1: skip the update (latency-floor measurement; results invalid)
-  long long* trace;              // optional event timeline (globaltimer ns), see mpgabor_set_trace
-  long long trace_it0;
-  int trace_n, trace_slots;
   int spec;                      // multi-selection: candidates per round (1..multi_max_batch())
   void* backup;                  // multi-selection: per-CTA tile backups [C][bk_cap][TW] (cplx<R>)
   long long bk_cap;              // items per CTA per round the backup holds
@@ -92,11 +89,6 @@ int multi_max_batch();
 cudaError_t launch_multi_loop(const LoopParams& P, bool f64, int threads, cudaStream_t st);
 int multi_max_cluster(bool f64, bool srec, int TW, int threads, size_t smem);
 
-// alternative loop kernel (mplean.cu): geometry once per CTA into row descriptors,
-// work items = row segments; selected with profile-mode bit 2
-size_t lean_smem_bytes(const LoopParams& P, bool f64);
-cudaError_t launch_lean_loop(const LoopParams& P, bool f64, int threads, cudaStream_t st);
-int lean_max_cluster(bool f64, bool srec, int TW, int threads, size_t smem);
 
 // synthesis (synth.cu)
 cudaError_t launch_synth_scatter(const AtomOut* atoms, int64_t n_atoms, const DictGeo* dg_dev, int W, double2* sol,

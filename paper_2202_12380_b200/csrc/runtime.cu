@@ -74,7 +74,7 @@ struct mpgabor {
   int TW = 64, srec = 0;
   int run_threads = 512;  // threads of the planned loop launch
   int batch = 0;          // candidates per round: 0 auto (multi-selection, multi_max_batch()), 1 one selection
-  int kind = 2;           // loop kernel: 0 mploop.cu, 1 mplean.cu, 2 mpmulti.cu
+  int kind = 2;           // loop kernel: 0 mploop.cu, 2 mpmulti.cu
   bool force_single = false;  // multi-selection impossible for this layout: use mploop.cu
 
   // per-length layout
@@ -91,9 +91,6 @@ struct mpgabor {
   DevBuf sol, frames, hx, hatoms, henergy, hy;
 
   int prof_mode = 0;
-  long long trace_it0 = 0;
-  int trace_n = 0;
-  DevBuf trace;
   long long prof_host[32] = {};
   DevBuf prof;
   cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -198,7 +195,7 @@ extern "C" void mpgabor_destroy(mpgabor* h) {
     cudaSetDevice(h->device);
     for (DevBuf* b : {&h->tw, &h->roots, &h->win, &h->kern, &h->boxcopy, &h->d_pairs, &h->rho, &h->rho_meta,
                       &h->Hscratch, &h->mxbox, &h->d_geo, &h->grid, &h->rec, &h->xp, &h->partial, &h->flag,
-                      &h->E0, &h->result, &h->sol, &h->frames, &h->hx, &h->hatoms, &h->henergy, &h->hy, &h->prof, &h->d_own, &h->trace, &h->backup})
+                      &h->E0, &h->result, &h->sol, &h->frames, &h->hx, &h->hatoms, &h->henergy, &h->hy, &h->prof, &h->d_own, &h->backup})
       b->release();
     for (auto e : h->ev)
       if (e) cudaEventDestroy(e);
@@ -538,13 +535,12 @@ static size_t plan_loop(mpgabor* h, int TW, int srec, int C) {
     n = (n + 31) / 32;
   }
   P.nlev = nl;
-  // loop kernel: 2 = mpmulti.cu (default), 0 = mploop.cu (batch 1), 1 = mplean.cu (profile-mode bit 2)
-  const int kind = (h->prof_mode & 4) ? 1 : ((h->batch == 1 || h->force_single || (h->batch == 0 && !auto_multi(h))) ? 0 : 2);
+  // loop kernel: 2 = mpmulti.cu, 0 = mploop.cu (batch 1, or the automatic choice)
+  const int kind = (h->batch == 1 || h->force_single || (h->batch == 0 && !auto_multi(h))) ? 0 : 2;
   h->kind = kind;
   h->run_threads = h->threads;
   P.spec = h->batch == 0 ? multi_max_batch() : h->batch;
-  P.smem_bytes = kind == 1 ? lean_smem_bytes(P, h->f64())
-                           : (kind == 2 ? multi_smem_bytes(P, h->f64()) : loop_smem_bytes(P, h->f64()));
+  P.smem_bytes = kind == 2 ? multi_smem_bytes(P, h->f64()) : loop_smem_bytes(P, h->f64());
   return P.smem_bytes;
 }
 
@@ -596,9 +592,8 @@ static int ensure_layout(mpgabor* h, int64_t Ls) {
         why = "shared memory " + std::to_string(smem) + " B";
         break;  // smaller clusters need more per-CTA memory
       }
-      const int cmax = h->kind == 1   ? lean_max_cluster(h->f64(), c.srec, c.TW, h->run_threads, smem)
-                       : h->kind == 2 ? multi_max_cluster(h->f64(), c.srec, c.TW, h->run_threads, smem)
-                                      : loop_max_cluster(h->f64(), c.srec, c.TW, h->run_threads, smem);
+      const int cmax = h->kind == 2 ? multi_max_cluster(h->f64(), c.srec, c.TW, h->run_threads, smem)
+                                    : loop_max_cluster(h->f64(), c.srec, c.TW, h->run_threads, smem);
       if (cmax >= C) {
         ok = true;
         break;
@@ -732,16 +727,6 @@ extern "C" int mpgabor_run(mpgabor* h, const double* x_dev, int64_t Ls, int64_t 
   P.sol = reinterpret_cast<double2*>(coef_dev);
   P.result = h->result.as<LoopResult>();
   P.floor_mode = (h->prof_mode & 2) ? 1 : 0;
-  P.trace = nullptr;
-  P.trace_it0 = h->trace_it0;
-  P.trace_n = h->trace_n;
-  P.trace_slots = 13 + h->run_threads / 32;
-  if (h->trace_n > 0) {
-    const size_t tb = sizeof(long long) * (size_t)h->trace_n * P.C * P.trace_slots;
-    TRY_CUDA(h, h->trace.ensure(tb));
-    TRY_CUDA(h, cudaMemsetAsync(h->trace.p, 0, tb, st));
-    P.trace = h->trace.as<long long>();
-  }
   P.prof = nullptr;
   if (h->prof_mode & 1) {
     TRY_CUDA(h, h->prof.ensure(sizeof(long long) * 32));
@@ -750,9 +735,7 @@ extern "C" int mpgabor_run(mpgabor* h, const double* x_dev, int64_t Ls, int64_t 
   }
   TRY_CUDA(h, cudaEventRecord(h->ev[3], st));
   P.backup = h->backup.p;
-  if (h->kind == 1)
-    TRY_LAUNCH(h, 1, launch_lean_loop(P, h->f64(), h->run_threads, st));
-  else if (h->kind == 2)
+  if (h->kind == 2)
     TRY_LAUNCH(h, 1, launch_multi_loop(P, h->f64(), h->run_threads, st));
   else
     TRY_LAUNCH(h, 1, launch_mp_loop(P, h->f64(), h->run_threads, st));
@@ -799,32 +782,9 @@ extern "C" int mpgabor_set_batch(mpgabor* h, int32_t max_batch) {
   return MPG_OK;
 }
 
-extern "C" int mpgabor_set_trace(mpgabor* h, int64_t it0, int32_t n) {
-  if (!h || it0 < 0 || n < 0) return MPG_EINVAL;
-  h->trace_it0 = it0;
-  h->trace_n = n;
-  return MPG_OK;
-}
-
-extern "C" int mpgabor_last_trace(mpgabor* h, int64_t* host, int64_t cap, int32_t* slots, int32_t* ctas) {
-  if (!h) return MPG_EINVAL;
-  const int S = 13 + h->run_threads / 32;
-  if (slots) *slots = S;
-  if (ctas) *ctas = h->lp.C;
-  const int64_t need = (int64_t)h->trace_n * h->lp.C * S;
-  if (host && need > 0) {
-    if (cap < need) return h->fail(MPG_EINVAL, "trace buffer too small");
-    int rc = enter_device(h);
-    if (rc) return rc;
-    TRY_CUDA(h, cudaMemcpy(host, h->trace.p, sizeof(int64_t) * need, cudaMemcpyDeviceToHost));
-  }
-  return MPG_OK;
-}
-
 extern "C" int mpgabor_set_profile(mpgabor* h, int32_t mode) {
   if (!h) return MPG_EINVAL;
-  if (mode < 0 || mode > 7) return h->fail(MPG_EINVAL, "profile mode must be in [0, 7]");
-  if ((mode & 4) != (h->prof_mode & 4)) h->L = -1;  // bit 2 switches the loop kernel: re-plan
+  if (mode < 0 || mode > 3) return h->fail(MPG_EINVAL, "profile mode must be in [0, 3]");
   h->prof_mode = mode;
   return MPG_OK;
 }

@@ -75,8 +75,6 @@ _SIGS = {
     "mpgabor_residual": ([_P, _P, _P], ctypes.c_int),
     "mpgabor_launch_count": ([_P, ctypes.POINTER(_I64)], ctypes.c_int),
     "mpgabor_set_profile": ([_P, _I32], ctypes.c_int),
-    "mpgabor_set_trace": ([_P, _I64, _I32], ctypes.c_int),
-    "mpgabor_last_trace": ([_P, _P, _I64, ctypes.POINTER(_I32), ctypes.POINTER(_I32)], ctypes.c_int),
     "mpgabor_last_profile": ([_P, ctypes.POINTER(_I64)], ctypes.c_int),
     "mpgabor_destroy": ([_P], None),
     "mpgabor_last_error": ([_P], ctypes.c_char_p),
@@ -224,19 +222,6 @@ def mpgabor_last_profile(h):
     c = (_I64 * 32)()
     _check(h, _lib.mpgabor_last_profile(h, c))
     return list(c)
-
-
-def mpgabor_set_trace(h, it0, n):
-    _check(h, _lib.mpgabor_set_trace(h, int(it0), int(n)))
-
-
-def mpgabor_last_trace(h, n):
-    S, Cn = _I32(), _I32()
-    _check(h, _lib.mpgabor_last_trace(h, None, 0, ctypes.byref(S), ctypes.byref(Cn)))
-    buf = np.zeros(n * S.value * Cn.value, dtype=np.int64)
-    _check(h, _lib.mpgabor_last_trace(h, ctypes.c_void_p(buf.ctypes.data), buf.size, ctypes.byref(S),
-                                      ctypes.byref(Cn)))
-    return buf.reshape(n, Cn.value, S.value)
 
 
 def mpgabor_destroy(h):
