@@ -97,6 +97,22 @@ def touched_per_atom(mp, dicts, atoms):
 mp_boxes = {}
 
 
+def loop_traffic(config, prec, kernel):
+    """DRAM bytes (read + write) of one launch of the loop kernel from the committed ncu
+    --set full capture (profiles/*loop_traffic.json), or None."""
+    import glob
+    key = f"{config}/{prec}/{kernel}"
+    for fn in sorted(glob.glob(os.path.join(ROOT, "profiles", "*loop_traffic.json")), reverse=True):
+        try:
+            d = json.load(open(fn))
+        except Exception:  # noqa: BLE001
+            continue
+        if key in d:
+            e = d[key]
+            return int(e["dram_read_bytes"] + e["dram_write_bytes"]), os.path.relpath(fn, ROOT) + ": " + e["source"]
+    return None, None
+
+
 # ---------------------------------------------------------------------------
 # clocks during the timed region
 # ---------------------------------------------------------------------------
@@ -298,6 +314,8 @@ def run_native(args, cfg, rank, world, local_rank):
     loop_mean_ms = float(np.mean(loop_ms))
     peak, peak_kind = peaks()
     achieved = alg_bytes / (loop_mean_ms * 1e-3) / 1e9
+    kernel = "mp_loop_kernel" if out.rounds == out.n + 1 else "mp_multi_kernel"
+    traffic, traffic_src = loop_traffic(cfg.name, args.precision, kernel)
 
     # end to end through the host-buffer C-ABI call (pinned host memory)
     import torch as _t
@@ -337,8 +355,9 @@ def run_native(args, cfg, rank, world, local_rank):
                    "phase_ms": {"dgt": dgt_ms, "init": init_ms, "loop": one_loop_ms},
                    "wall_s": wall_s},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
-                     "kernel": "mp_loop_kernel", "alg_bytes_per_launch": alg_bytes,
+                     "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                     "peak_kind": peak_kind, "kernel": kernel, "rounds_per_launch": int(out.rounds),
+                     "alg_bytes_per_launch": alg_bytes,
                      "touched_per_iter": float(touched.mean()), "bytes_per_touched": bpc,
                      "us_per_iter": 1e3 * loop_mean_ms / max(1, out.n)},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": cfg.Ls * 8, "d2h_bytes_per_step": d2h},
