@@ -150,7 +150,8 @@ int mpgabor_decompose_host(mpgabor* h, const double* x_host, int64_t Ls, int64_t
                            mpg_result* res, void* cuda_stream);
 
 /* Launch tuning of the persistent loop: cluster size (1..16 CTAs, one per SM,
- * power of two), threads per CTA (128..512, multiple of 32), tile width in
+ * power of two; or 32, 64, 128: the one-selection loop as a cooperative grid of
+ * that many CTAs exchanging their roots through global memory), threads per CTA (128..512, multiple of 32), tile width in
  * bins (32, 64 or 128), tile-record placement (1 shared memory, 2 global
  * memory).  0 selects automatically (largest cluster; shared records with
  * tile width 64, else 128, else global records).  Takes effect at the next run. */

@@ -70,6 +70,8 @@ struct LoopParams {
   LoopResult* result;
   long long* prof;               // optional [8] clock64 phase sums (rank 0, thread 0), [7] = iterations
   int floor_mode;                // 1: skip the update (latency-floor measurement; results invalid)
+  void* gx_rec;                  // one-selection kernel, grid mode: Rec<R>[2][C] roots in global memory (else null)
+  unsigned long long* gx_stamp;  // [2][C] iteration stamps of gx_rec (zeroed before the launch)
   int spec;                      // multi-selection: candidates per round (1..multi_max_batch())
   void* backup;                  // multi-selection: per-CTA tile backups [C][bk_cap][TW] (cplx<R>)
   long long bk_cap;              // items per CTA per round the backup holds
@@ -79,7 +81,8 @@ struct LoopParams {
 // default loop kernel (mploop.cu)
 size_t loop_smem_bytes(const LoopParams& P, bool f64);
 cudaError_t launch_mp_loop(const LoopParams& P, bool f64, int threads, cudaStream_t st);
-int loop_max_cluster(bool f64, bool srec, int TW, int threads, size_t smem);
+// gx: the global-exchange grid kernel; returns its co-resident CTA count
+int loop_max_cluster(bool f64, bool srec, int TW, int threads, size_t smem, bool gx = false);
 
 // exact multi-selection loop kernel (mpmulti.cu, the default): MULTI_K = length of
 // every CTA's published top-K tile list

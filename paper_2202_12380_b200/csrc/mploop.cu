@@ -87,13 +87,27 @@ __host__ __device__ inline Smem smem_layout(const LoopParams& P, size_t recsz) {
   return s;
 }
 
-template <typename R, int TW, bool SREC>
+// global-exchange helpers (GX): a CTA's root record and its iteration stamp in global
+// memory; the stamp is written with release and polled with acquire semantics (gpu scope)
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// GX = false: one thread-block cluster of C <= 16 CTAs exchanging roots through
+// distributed shared memory.  GX = true: a cooperative grid of C CTAs (C a power of
+// two up to 128, one per SM) exchanging roots through global memory (release/acquire
+// stamps); everything else is identical.
+template <typename R, int TW, bool SREC, bool GX>
 __global__ void __launch_bounds__(512, 1) mp_loop_kernel(const LoopParams P) {
   using C2 = typename cplx<R>::t;
   using RecT = Rec<R>;
-  cg::cluster_group cluster = cg::this_cluster();
   const int C = P.C, lgC = ilog2(P.C);
-  const int rank = (int)cluster.block_rank();
+  const int rank = GX ? (int)blockIdx.x : (int)cg::this_cluster().block_rank();
   const int W = P.W;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
   constexpr int LGTW = TW == 32 ? 5 : (TW == 64 ? 6 : 7);
@@ -162,8 +176,10 @@ __global__ void __launch_bounds__(512, 1) mp_loop_kernel(const LoopParams P) {
     sel->E[0] = P.E0;
     sel->stop = 0;
   }
-  cluster.sync();
+  if constexpr (GX) __syncthreads();
+  else cg::this_cluster().sync();
   // warp 0: scan the top level, push the root into slot `slot` of every CTA's mailbox
+  unsigned long long stampnext = 1;  // GX: stamp of the root published next (= iteration + 1)
   auto publish_root = [&](int slot) {
     const int top = P.nlev - 1;
     const RecT* tl = lev + P.lev_off[top];
@@ -173,8 +189,14 @@ __global__ void __launch_bounds__(512, 1) mp_loop_kernel(const LoopParams P) {
       if (better(r.s, r.p, b.s, b.p)) b = r;
     }
     b = warp_best(b);
-    if (lane < C)
+    if constexpr (GX) {
+      if (lane == 0) {  // record, then its stamp (release): iteration `stamp - 1` may read it
+        reinterpret_cast<RecT*>(P.gx_rec)[slot * C + rank] = b;
+        st_release_u64(P.gx_stamp + slot * C + rank, stampnext);
+      }
+    } else if (lane < C) {
       push_record(b, mapa(smem_addr(&mail[slot * MAX_CLUSTER + rank]), lane), mapa(smem_addr(&mbar[slot]), lane));
+    }
   };
   if (warp == 0) publish_root(0);
   long long it = 0;
@@ -191,11 +213,26 @@ __global__ void __launch_bounds__(512, 1) mp_loop_kernel(const LoopParams P) {
   for (;; ++it) {
     const int par = (int)(it & 1);
     // ---- A. selection (warps 0, 1); scalar step (warp 0); geometry (warp 1) ----
-    if (warp < 2) mbar_wait(smem_addr(&mbar[par]), (uint32_t)((it >> 1) & 1));
+    if (!GX && warp < 2) mbar_wait(smem_addr(&mbar[par]), (uint32_t)((it >> 1) & 1));
+    if (GX && warp < 2) {  // every CTA's root of this iteration: stamps == it + 1
+      const unsigned long long want = (unsigned long long)it + 1;
+      for (int c = lane; c < C; c += 32)
+        while (ld_acquire_u64(P.gx_stamp + par * C + c) != want) {
+        }
+      __syncwarp();
+    }
     PROF_MARK(0);
     if (warp < 2) {
-      const RecT cand = lane < C ? mail[par * MAX_CLUSTER + lane] : empty_rec(R(0));
-      if (warp == 0 && lane == 0) mbar_arm(smem_addr(&mbar[par]), C * recbytes);  // slot reused at it + 2
+      RecT cand = empty_rec(R(0));
+      if constexpr (GX) {
+        for (int c = lane; c < C; c += 32) {
+          const RecT r = reinterpret_cast<const RecT*>(P.gx_rec)[par * C + c];
+          if (better(r.s, r.p, cand.s, cand.p)) cand = r;
+        }
+      } else {
+        if (lane < C) cand = mail[par * MAX_CLUSTER + lane];
+        if (warp == 0 && lane == 0) mbar_arm(smem_addr(&mbar[par]), C * recbytes);  // slot reused at it + 2
+      }
       const RecT best = warp_best(cand);
       const double Ecur = sel->E[par];
       int st = 0;
@@ -422,6 +459,7 @@ __global__ void __launch_bounds__(512, 1) mp_loop_kernel(const LoopParams P) {
           __syncwarp();
         }
       }
+      stampnext = (unsigned long long)it + 2;
       publish_root(par ^ 1);
       if (lane == 0)
         for (int l = 0; l < P.nlev; ++l) cnt[l] = 0;
@@ -438,24 +476,29 @@ __global__ void __launch_bounds__(512, 1) mp_loop_kernel(const LoopParams P) {
     P.prof[7] = it;
   }
 #undef PROF_MARK
-  cluster.sync();  // keep every CTA's shared memory alive until all remote stores are done
+  if constexpr (!GX) cg::this_cluster().sync();  // keep shared memory alive until all remote stores are done
 }
 
-template <typename R, int TW, bool SREC>
+template <typename R, int TW, bool SREC, bool GX>
 cudaError_t launch_t(const LoopParams& P, int threads, cudaStream_t st) {
-  auto kfn = mp_loop_kernel<R, TW, SREC>;
+  auto kfn = mp_loop_kernel<R, TW, SREC, GX>;
   CUDA_OK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem_bytes));
-  if (P.C > 8) CUDA_OK(cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  if (!GX && P.C > 8) CUDA_OK(cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(P.C, 1, 1);
   cfg.blockDim = dim3(threads, 1, 1);
   cfg.dynamicSmemBytes = P.smem_bytes;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = P.C;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
+  if (GX) {  // all CTAs co-resident: they spin on each other's stamps
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+  } else {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = P.C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+  }
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kfn, P);
@@ -463,7 +506,7 @@ cudaError_t launch_t(const LoopParams& P, int threads, cudaStream_t st) {
 
 template <typename R, int TW, bool SREC>
 int max_cluster_t(int threads, size_t smem) {
-  auto kfn = mp_loop_kernel<R, TW, SREC>;
+  auto kfn = mp_loop_kernel<R, TW, SREC, false>;
   if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
       cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
     cudaGetLastError();
@@ -488,21 +531,38 @@ int max_cluster_t(int threads, size_t smem) {
   return 0;
 }
 
-template <typename R, bool SREC>
+// co-resident CTAs of the global-exchange kernel (one per SM at most)
+template <typename R, int TW, bool SREC>
+int max_grid_t(int threads, size_t smem) {
+  auto kfn = mp_loop_kernel<R, TW, SREC, true>;
+  if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  int per_sm = 0, dev = 0, sms = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, threads, smem) != cudaSuccess ||
+      cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return per_sm * sms;
+}
+
+template <typename R, bool SREC, bool GX>
 cudaError_t launch_r(const LoopParams& P, int threads, cudaStream_t st) {
   switch (P.TW) {
-    case 32: return launch_t<R, 32, SREC>(P, threads, st);
-    case 64: return launch_t<R, 64, SREC>(P, threads, st);
-    case 128: return launch_t<R, 128, SREC>(P, threads, st);
+    case 32: return launch_t<R, 32, SREC, GX>(P, threads, st);
+    case 64: return launch_t<R, 64, SREC, GX>(P, threads, st);
+    case 128: return launch_t<R, 128, SREC, GX>(P, threads, st);
   }
   return cudaErrorInvalidValue;
 }
 template <typename R, bool SREC>
-int max_cluster_r(int TW, int threads, size_t smem) {
+int max_cluster_r(int TW, int threads, size_t smem, bool gx) {
   switch (TW) {
-    case 32: return max_cluster_t<R, 32, SREC>(threads, smem);
-    case 64: return max_cluster_t<R, 64, SREC>(threads, smem);
-    case 128: return max_cluster_t<R, 128, SREC>(threads, smem);
+    case 32: return gx ? max_grid_t<R, 32, SREC>(threads, smem) : max_cluster_t<R, 32, SREC>(threads, smem);
+    case 64: return gx ? max_grid_t<R, 64, SREC>(threads, smem) : max_cluster_t<R, 64, SREC>(threads, smem);
+    case 128: return gx ? max_grid_t<R, 128, SREC>(threads, smem) : max_cluster_t<R, 128, SREC>(threads, smem);
   }
   return 0;
 }
@@ -514,11 +574,16 @@ size_t loop_smem_bytes(const LoopParams& P, bool f64) {
 }
 
 cudaError_t launch_mp_loop(const LoopParams& P, bool f64, int threads, cudaStream_t st) {
-  if (f64) return P.srec ? launch_r<double, true>(P, threads, st) : launch_r<double, false>(P, threads, st);
-  return P.srec ? launch_r<float, true>(P, threads, st) : launch_r<float, false>(P, threads, st);
+  const bool gx = P.gx_rec != nullptr;
+  if (gx) {
+    if (f64) return P.srec ? launch_r<double, true, true>(P, threads, st) : launch_r<double, false, true>(P, threads, st);
+    return P.srec ? launch_r<float, true, true>(P, threads, st) : launch_r<float, false, true>(P, threads, st);
+  }
+  if (f64) return P.srec ? launch_r<double, true, false>(P, threads, st) : launch_r<double, false, false>(P, threads, st);
+  return P.srec ? launch_r<float, true, false>(P, threads, st) : launch_r<float, false, false>(P, threads, st);
 }
 
-int loop_max_cluster(bool f64, bool srec, int TW, int threads, size_t smem) {
-  if (f64) return srec ? max_cluster_r<double, true>(TW, threads, smem) : max_cluster_r<double, false>(TW, threads, smem);
-  return srec ? max_cluster_r<float, true>(TW, threads, smem) : max_cluster_r<float, false>(TW, threads, smem);
+int loop_max_cluster(bool f64, bool srec, int TW, int threads, size_t smem, bool gx) {
+  if (f64) return srec ? max_cluster_r<double, true>(TW, threads, smem, gx) : max_cluster_r<double, false>(TW, threads, smem, gx);
+  return srec ? max_cluster_r<float, true>(TW, threads, smem, gx) : max_cluster_r<float, false>(TW, threads, smem, gx);
 }

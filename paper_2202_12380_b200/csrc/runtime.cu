@@ -76,6 +76,8 @@ struct mpgabor {
   int batch = 0;          // candidates per round: 0 auto (multi-selection, multi_max_batch()), 1 one selection
   int kind = 2;           // loop kernel: 0 mploop.cu, 2 mpmulti.cu
   bool force_single = false;  // multi-selection impossible for this layout: use mploop.cu
+  bool gx = false;            // one-selection kernel as a cooperative grid (> 16 CTAs, global exchange)
+  DevBuf gxrec, gxstamp;
 
   // per-length layout
   int64_t L = -1, Ls_cached = -1;
@@ -195,7 +197,7 @@ extern "C" void mpgabor_destroy(mpgabor* h) {
     cudaSetDevice(h->device);
     for (DevBuf* b : {&h->tw, &h->roots, &h->win, &h->kern, &h->boxcopy, &h->d_pairs, &h->rho, &h->rho_meta,
                       &h->Hscratch, &h->mxbox, &h->d_geo, &h->grid, &h->rec, &h->xp, &h->partial, &h->flag,
-                      &h->E0, &h->result, &h->sol, &h->frames, &h->hx, &h->hatoms, &h->henergy, &h->hy, &h->prof, &h->d_own, &h->backup})
+                      &h->E0, &h->result, &h->sol, &h->frames, &h->hx, &h->hatoms, &h->henergy, &h->hy, &h->prof, &h->d_own, &h->backup, &h->gxrec, &h->gxstamp})
       b->release();
     for (auto e : h->ev)
       if (e) cudaEventDestroy(e);
@@ -427,8 +429,8 @@ extern "C" int mpgabor_layout(const mpgabor* h, int64_t Ls, int64_t* L_pad, int6
 extern "C" int mpgabor_set_launch(mpgabor* h, int32_t cluster, int32_t threads, int32_t tile_width,
                                   int32_t records) {
   if (!h) return MPG_EINVAL;
-  if (cluster < 0 || cluster > 16 || (cluster && (cluster & (cluster - 1))))
-    return h->fail(MPG_EINVAL, "cluster must be 0 or a power of two <= 16");
+  if (cluster < 0 || cluster > 128 || (cluster && (cluster & (cluster - 1))))
+    return h->fail(MPG_EINVAL, "cluster must be 0, a power of two <= 16 (one cluster) or 32/64/128 (grid)");
   if (threads && (threads < 128 || threads > 512 || threads % 32))
     return h->fail(MPG_EINVAL, "threads must be in [128,512], multiple of 32");
   if (tile_width && tile_width != 32 && tile_width != 64 && tile_width != 128)
@@ -483,7 +485,7 @@ static int plan_grids(mpgabor* h, int64_t L, int TW) {
 // near C2 (2,176) and loses on C3/C4 (18.5k / 56k).  Estimate the mean update size
 // from the kernel boxes (subsampled per target, averaged over the selected dictionary)
 // and require it to be a small fraction of the grid.
-static bool auto_multi(const mpgabor* h) {
+static double mean_update(const mpgabor* h) {
   const int W = h->W;
   double sum = 0.0;
   for (int u = 0; u < W; ++u)
@@ -491,7 +493,11 @@ static bool auto_multi(const mpgabor* h) {
       const PairGeo& pg = h->pairs[u * W + v];
       sum += (double)pg.nnu / pg.s_n * ((double)pg.nmu / pg.s_m);
     }
-  const double per_atom = sum / W;
+  return sum / W;
+}
+
+static bool auto_multi(const mpgabor* h) {
+  const double per_atom = mean_update(h);
   // rounds need independent atoms: small patches relative to the grid (C0's patch
   // covers 2.6 % of its grid and gives ~2 atoms per round)
   return per_atom < 1500.0 && per_atom < 0.005 * (double)h->P_R;
@@ -578,6 +584,15 @@ static int ensure_layout(mpgabor* h, int64_t Ls) {
     if (L / h->dicts[v].a >= (1 << 20)) h->force_single = true;
   for (int i = 0; i < W * W; ++i)
     if ((h->pairs[i].nnu + h->pairs[i].s_n - 1) / h->pairs[i].s_n >= (1 << 12)) h->force_single = true;
+  // automatic grid mode: very wide updates (C4: ~54k coefficients per atom) spread over 64
+  // CTAs beat one 16-CTA cluster despite the global-memory exchange
+  const bool single = h->batch == 1 || (h->batch == 0 && !auto_multi(h));
+  const bool try_grid = h->cluster_req == 0 && single && mean_update(h) > 30000.0;
+  const bool force_single0 = h->force_single;
+  for (int pass = try_grid ? 0 : 1; pass < 2 && !ok; ++pass) {
+  const int creq = pass == 0 ? 64 : h->cluster_req;
+  h->gx = creq > MAX_CLUSTER;
+  h->force_single = force_single0 || h->gx;  // grid mode: one-selection kernel
   for (int attempt = 0; attempt < 2 && !ok; ++attempt) {
   if (attempt == 1) {
     if (h->kind != 2) break;
@@ -586,26 +601,27 @@ static int ensure_layout(mpgabor* h, int64_t Ls) {
   for (const Cand& c : cands) {
     int rc = plan_grids(h, L, c.TW);
     if (rc) return rc;
-    for (int C = h->cluster_req ? h->cluster_req : MAX_CLUSTER; C >= 1; C >>= 1) {
+    for (int C = creq ? creq : MAX_CLUSTER; C >= 1; C >>= 1) {
       const size_t smem = plan_loop(h, c.TW, c.srec, C);
       if (smem > 227 * 1024) {
         why = "shared memory " + std::to_string(smem) + " B";
         break;  // smaller clusters need more per-CTA memory
       }
       const int cmax = h->kind == 2 ? multi_max_cluster(h->f64(), c.srec, c.TW, h->run_threads, smem)
-                                    : loop_max_cluster(h->f64(), c.srec, c.TW, h->run_threads, smem);
+                                    : loop_max_cluster(h->f64(), c.srec, c.TW, h->run_threads, smem, h->gx);
       if (cmax >= C) {
         ok = true;
         break;
       }
       why = "cluster of " + std::to_string(C) + " not schedulable";
-      if (h->cluster_req) break;
+      if (creq) break;
     }
     if (ok) {
       h->TW = c.TW;
       h->srec = c.srec;
       break;
     }
+  }
   }
   }
   if (!ok) return h->fail(MPG_ECUDA, "no launch plan for the MP loop: " + why);
@@ -623,6 +639,10 @@ static int ensure_layout(mpgabor* h, int64_t Ls) {
   TRY_CUDA(h, h->flag.ensure(sizeof(int)));
   TRY_CUDA(h, h->E0.ensure(sizeof(double)));
   TRY_CUDA(h, h->result.ensure(sizeof(LoopResult)));
+  if (h->gx) {
+    TRY_CUDA(h, h->gxrec.ensure((h->f64() ? sizeof(Rec<double>) : sizeof(Rec<float>)) * 2 * P.C));
+    TRY_CUDA(h, h->gxstamp.ensure(sizeof(unsigned long long) * 2 * P.C));
+  }
   if (h->kind == 2) {
     // roll-back backups: per CTA and round at most spec x max_u sum_v (rows/C + 1) x (hull tiles)
     // items (rows = alignment-class sub-box rows, hull tiles <= cols/TW + 1)
@@ -735,6 +755,13 @@ extern "C" int mpgabor_run(mpgabor* h, const double* x_dev, int64_t Ls, int64_t 
   }
   TRY_CUDA(h, cudaEventRecord(h->ev[3], st));
   P.backup = h->backup.p;
+  P.gx_rec = nullptr;
+  P.gx_stamp = nullptr;
+  if (h->gx) {  // stamps start at 0: the first roots carry stamp 1
+    TRY_CUDA(h, cudaMemsetAsync(h->gxstamp.p, 0, sizeof(unsigned long long) * 2 * P.C, st));
+    P.gx_rec = h->gxrec.p;
+    P.gx_stamp = h->gxstamp.as<unsigned long long>();
+  }
   if (h->kind == 2)
     TRY_LAUNCH(h, 1, launch_multi_loop(P, h->f64(), h->run_threads, st));
   else

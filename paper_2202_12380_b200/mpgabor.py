@@ -15,7 +15,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmpgabor.so")
+LIB_PATH = os.environ.get("MPGABOR_LIB") or os.path.join(_HERE, "libmpgabor.so")  # override: A/B timing of builds
 
 MPG_WIN_HANN, MPG_WIN_BLACKMAN, MPG_WIN_GAUSS = 1, 2, 3
 MPG_F64, MPG_F32 = 0, 1

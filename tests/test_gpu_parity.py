@@ -254,6 +254,27 @@ def test_multi_selection_bitwise_identical(mpg, name, prec, K):
     mp.close()
 
 
+@pytest.mark.parametrize("name,prec,K", [("C1", "f64", 3000), ("C2", "f32", 3000), ("C4", "f64", 1500)])
+def test_grid_mode_bitwise_identical(mpg, name, prec, K):
+    # the one-selection loop as a cooperative grid of 32/64/128 CTAs (global-memory root
+    # exchange) gives the decomposition of the 16-CTA cluster, bit for bit
+    cfg = CONFIGS[name]
+    x, S = setup_of(name)
+    xd = torch.from_numpy(x).cuda()
+    mp = mpg.MPGabor(cfg.dicts, cfg.thr, prec)
+    mp.set_batch(1)
+    mp.set_launch(16, 0, 0, 0)
+    ref = mp.run(xd, K, cfg.errdb)
+    res_ref = mp.residual(cfg.Ls).cpu().numpy()
+    for C in (32, 64, 128):
+        mp.set_launch(C, 0, 0, 0)
+        out = mp.run(xd, K, cfg.errdb)
+        assert mp.launch_info()["cluster"] == C
+        assert out.atoms.tobytes() == ref.atoms.tobytes() and out.energy.tobytes() == ref.energy.tobytes(), C
+        assert np.array_equal(mp.residual(cfg.Ls).cpu().numpy(), res_ref), C
+    mp.close()
+
+
 def test_multi_selection_solution_vector(mpg):
     # the solution vector c (Alg. 1 step 2a) only accumulates verified atoms
     cfg = CONFIGS["C1"]
