@@ -90,7 +90,8 @@ def error_tolerance(errdb: float, E0: float) -> float:
 
 
 def mp_run(setup, maxit: int, errdb: float = -math.inf, full_scan: bool = False,
-           want_gaps: bool = True) -> MpResult:
+           want_gaps: bool = True, etol: float | None = None) -> MpResult:
+    """Alg. 1 on the setup's grids; ``etol`` (absolute energy level) overrides errdb."""
     lib = _load()
     lay = setup.lay
     W = len(setup.dicts)
@@ -108,7 +109,7 @@ def mp_run(setup, maxit: int, errdb: float = -math.inf, full_scan: bool = False,
     n_done = ctypes.c_int64(0)
     stop = ctypes.c_int32(0)
     rc = lib.orc_mp_run(W, dd, kk, res.ctypes.data, sol.ctypes.data, maxit,
-                        error_tolerance(errdb, setup.E0), setup.E0, int(full_scan),
+                        error_tolerance(errdb, setup.E0) if etol is None else etol, setup.E0, int(full_scan),
                         atoms.ctypes.data, energy.ctypes.data,
                         gaps.ctypes.data if want_gaps else None,
                         ctypes.byref(n_done), ctypes.byref(stop))
@@ -121,3 +122,70 @@ def mp_run(setup, maxit: int, errdb: float = -math.inf, full_scan: bool = False,
     index = off[at["w"]] + at["n"].astype(np.int64) * MR[at["w"]] + at["m"]
     return MpResult(at, energy[: n + 1].copy(), gaps[:n].copy() if want_gaps else None,
                     stop.value, res, sol, index)
+
+
+@dataclass
+class ResetResult:
+    atoms: np.ndarray        # ATOM_DTYPE[n], all passes in order
+    energy: np.ndarray       # E_0 .. E_n: the true residual energy at every pass start, estimates inside
+    stop: int
+    passes: int
+    residual: np.ndarray     # final signal-domain residual r_out (length L)
+    index: np.ndarray
+
+    @property
+    def n(self):
+        return self.atoms.size
+
+    @property
+    def stop_name(self):
+        return STOP_NAMES.get(self.stop, "?")
+
+
+def mp_run_reset(x, dicts, thr, maxit: int, errdb: float, reset_every: int, K=None) -> ResetResult:
+    """Approximate coefficient-domain MP with reset, Alg. 2.
+
+    Outer loop: while the stopping criterion (maxit atoms; true residual energy
+    E_out <= 10^(errdb/10) ||x||^2) is not met, run Alg. 1 from
+    c^ = D^* r_out with E_k starting at E_out (step 1), until the reset criterion:
+    ``reset_every`` selections, or the inner estimate reaching the stop level or a
+    negative estimate; a zero largest score ends the run.  Then
+    c_out += c, r_out -= D c (synthesis, Eq. (18)) and E_out = ||r_out||^2 (step 2).
+    The problem lives on the zero-padded signal (reading Z3): r_out has length L.
+    """
+    from . import gabor
+    dicts = tuple(dicts)
+    Ls = x.size
+    lay = gabor.layout(dicts, Ls)
+    L = lay.L
+    if K is None:
+        K = gabor.kernels(dicts, thr)
+    r = np.zeros(L)
+    r[:Ls] = x
+    E0 = float(np.dot(x, x))
+    etol = error_tolerance(errdb, E0)
+    atoms, energy = [], [E0]
+    k, passes, stop = 0, 0, 1
+    while True:
+        if k >= maxit:
+            stop = 1
+            break
+        S = gabor.Setup.build(r, dicts, thr, K)          # c^ = D^* r_out, E_k = E_out = ||r_out||^2
+        energy[-1] = S.E0
+        inner = mp_run(S, min(int(reset_every), maxit - k), etol=etol, want_gaps=False)
+        passes += 1
+        if inner.n == 0:
+            stop = inner.stop                             # errtol on E_out, or zero score
+            break
+        atoms.append(inner.atoms)
+        energy.extend(inner.energy[1:].tolist())
+        r = r - gabor.synthesize(inner.atoms, dicts, L, L)   # r_out -= D c
+        k += inner.n
+        if inner.stop == 4:
+            stop = 4
+            break
+    at = np.concatenate(atoms) if atoms else np.zeros(0, dtype=ATOM_DTYPE)
+    off = np.asarray(lay.off)
+    MR = np.asarray(lay.MR)
+    index = off[at["w"]] + at["n"].astype(np.int64) * MR[at["w"]] + at["m"]
+    return ResetResult(at, np.asarray(energy), stop, passes, r, index)

@@ -164,3 +164,70 @@ def test_residual_at_one_by_one_equals_loop():
                                             rng.integers(0, S.lay.P, 40)]), 0, S.lay.P - 1))
     got = gabor.residual_at(S, r.atoms, pts)
     assert np.max(np.abs(got - r.res[pts])) < 1e-14 * math.sqrt(S.E0)
+
+
+# ---------------------------------------------------------------------------
+# Alg. 2: approximate coefficient-domain MP nested in resets
+# ---------------------------------------------------------------------------
+def _dense_energy(x, dicts, atoms, L):
+    """||x_pad - sum_atoms||^2 with materialised atoms (independent of gabor.synthesize):
+    c~ d for self-conjugate atoms, 2 Re(c~ d) for pairs (Eq. (18))."""
+    r = np.zeros(L)
+    r[: x.size] = x
+    for a in atoms:
+        d = dense.atom(dicts[int(a["w"])], int(a["m"]), int(a["n"]), L)
+        z = (a["re"] + 1j * a["im"]) * d
+        r -= z.real if a["flags"] & 1 else 2.0 * z.real
+    return float(np.dot(r, r))
+
+
+def test_reset_without_reset_equals_alg1():
+    cfg = CONFIGS["C0"]
+    x = signal(cfg)
+    r1 = loop.mp_run(oracle.Setup.build(x, cfg.dicts, cfg.thr), 300, cfg.errdb)
+    r2 = loop.mp_run_reset(x, cfg.dicts, cfg.thr, 300, cfg.errdb, reset_every=10**6)
+    assert r2.passes == 1 and r2.n == r1.n
+    assert r1.atoms.tobytes() == r2.atoms.tobytes() and np.array_equal(r1.energy, r2.energy)
+
+
+@pytest.mark.parametrize("every", [1, 7, 25])
+def test_reset_threshold_zero_equals_signal_mp(every):
+    # eps = 0: every pass is exact MP, so resets change nothing but rounding (Eq. (8))
+    dicts = (Dict(HANN, 16, 4, 16), Dict(HANN, 8, 2, 8))
+    x = random_signal(96, 21)
+    r = loop.mp_run_reset(x, dicts, 0.0, 60, -math.inf, every)
+    a_s, e_s, _, _, _ = dense.signal_mp(x, dicts, 60)
+    assert _seq(r.atoms) == _seq(a_s)
+    np.testing.assert_allclose(r.atoms["re"], a_s["re"], atol=1e-12)
+    np.testing.assert_allclose(r.energy, e_s, rtol=0, atol=1e-12 * e_s[0])
+
+
+def test_reset_pass_energies_are_true_residual_energies():
+    # at every pass start E_k = ||x - D c_out||^2 (Alg. 2 step 2d), recomputed from the
+    # atom list with materialised atoms; inside a pass E_k is the Eq. (20) estimate
+    dicts = (Dict(BLACKMAN, 32, 8, 32), Dict(HANN, 16, 4, 16))
+    x = random_signal(200, 5)          # ragged: padded to L = 224 (reading Z3)
+    lay = gabor.layout(dicts, x.size)
+    every = 9
+    r = loop.mp_run_reset(x, dicts, 1e-2, 45, -math.inf, every)
+    assert r.n == 45 and r.passes == 5
+    for k in range(0, r.n, every):
+        assert abs(r.energy[k] - _dense_energy(x, dicts, r.atoms[:k], lay.L)) <= 1e-11 * r.energy[0]
+    assert abs(float(np.dot(r.residual, r.residual)) - _dense_energy(x, dicts, r.atoms, lay.L)) <= 1e-11 * r.energy[0]
+
+
+def test_reset_recovers_truncation_drift():
+    # Theorem 2 (P:498-540): with a coarse Gram threshold the plain approximate loop
+    # stalls above the exact error, the reset loop keeps decreasing the true error
+    dicts = (Dict(HANN, 32, 8, 32), Dict(HANN, 16, 4, 16))
+    x = random_signal(256, 3)
+    lay = gabor.layout(dicts, x.size)
+    K = 150
+    plain = loop.mp_run(oracle.Setup.build(x, dicts, 0.3), K)
+    reset = loop.mp_run_reset(x, dicts, 0.3, K, -math.inf, 10)
+    e_plain = _dense_energy(x, dicts, plain.atoms, lay.L)
+    e_reset = float(np.dot(reset.residual, reset.residual))
+    assert e_reset < 0.5 * e_plain
+    # the true energies at the pass starts decrease
+    starts = reset.energy[::10][: reset.passes]
+    assert np.all(np.diff(starts) < 0)
