@@ -132,6 +132,22 @@ int mpgabor_run(mpgabor* h, const double* x_dev, int64_t Ls, int64_t maxit, doub
                 mpg_atom* atoms_dev, double* energy_dev, double* coef_dev, mpg_result* res,
                 void* cuda_stream);
 
+/* Approximate coefficient-domain MP with reset, Alg. 2: passes of the
+ * loop of mpgabor_run on the signal-domain residual r_out (x zero-padded to L_pad,
+ * DESIGN.md Z3).  Each pass starts from c^ = D^* r_out with E_k = ||r_out||^2 and runs
+ * until reset_every (>= 1) selections or an inner stop rule; then r_out -= D c
+ * (synthesis of the pass's atoms).  The run stops after maxit selections in total,
+ * when the true residual energy at a pass start is <= 10^(errdb/10) ||x||^2, or at
+ * a zero largest score.  Outputs as for mpgabor_run (atoms of all passes in order;
+ * energy_dev[k] is the true residual energy ||r_out||^2 at every pass start k and
+ * the Eq. (20) estimate inside a pass); res->E_final = energy_dev[n_atoms].  The
+ * solution vector is not produced (it is the sum of the atom list).  Synchronises
+ * cuda_stream. */
+int mpgabor_run_reset(mpgabor* h, const double* x_dev, int64_t Ls, int64_t maxit, double errdb,
+                      int64_t reset_every, mpg_atom* atoms_dev, double* energy_dev, mpg_result* res,
+                      void* cuda_stream);
+/* Number of passes of the last mpgabor_run_reset (host output). */
+int mpgabor_last_passes(const mpgabor* h, int32_t* passes);
 /* Synthesis of the approximation from an atom list (Eq. (18)):
  * y = sum_atoms c~ d (self-conjugate) or 2 Re(c~ d) (pairs), on L_pad samples,
  * truncated to Ls and written to y_dev (device fp64[Ls]).  atoms_dev: device

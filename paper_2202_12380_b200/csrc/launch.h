@@ -98,5 +98,6 @@ cudaError_t launch_synth_scatter(const AtomOut* atoms, int64_t n_atoms, const Di
                                  cudaStream_t st);
 cudaError_t launch_synth_frames(const double2* sol, const DictGeo& d, const double2* tw, int twres, double* frames,
                                 cudaStream_t st);
+cudaError_t launch_sub(double* r, const double* y, int64_t n, cudaStream_t st);  // r -= y
 cudaError_t launch_synth_ola(const double* frames, const DictGeo& d, const double* g, int64_t L, double* y,
                              int accumulate, cudaStream_t st);

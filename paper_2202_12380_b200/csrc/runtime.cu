@@ -91,6 +91,8 @@ struct mpgabor {
 
   // synth / host-api scratch
   DevBuf sol, frames, hx, hatoms, henergy, hy;
+  DevBuf rr, yy;          // resets: signal-domain residual r_out and the pass synthesis
+  int passes = 0;         // passes of the last mpgabor_run_reset
 
   int prof_mode = 0;
   long long prof_host[32] = {};
@@ -197,7 +199,7 @@ extern "C" void mpgabor_destroy(mpgabor* h) {
     cudaSetDevice(h->device);
     for (DevBuf* b : {&h->tw, &h->roots, &h->win, &h->kern, &h->boxcopy, &h->d_pairs, &h->rho, &h->rho_meta,
                       &h->Hscratch, &h->mxbox, &h->d_geo, &h->grid, &h->rec, &h->xp, &h->partial, &h->flag,
-                      &h->E0, &h->result, &h->sol, &h->frames, &h->hx, &h->hatoms, &h->henergy, &h->hy, &h->prof, &h->d_own, &h->backup, &h->gxrec, &h->gxstamp})
+                      &h->E0, &h->result, &h->sol, &h->frames, &h->hx, &h->hatoms, &h->henergy, &h->hy, &h->prof, &h->d_own, &h->backup, &h->gxrec, &h->gxstamp, &h->rr, &h->yy})
       b->release();
     for (auto e : h->ev)
       if (e) cudaEventDestroy(e);
@@ -680,9 +682,9 @@ extern "C" int mpgabor_launch_info(const mpgabor* h, int32_t* cluster, int32_t* 
 // ---------------------------------------------------------------------------
 // run
 // ---------------------------------------------------------------------------
-extern "C" int mpgabor_run(mpgabor* h, const double* x_dev, int64_t Ls, int64_t maxit, double errdb,
-                           mpg_atom* atoms_dev, double* energy_dev, double* coef_dev, mpg_result* res,
-                           void* stream) {
+// DGT + loop; etol_abs (nullable) replaces the stop level 10^(errdb/10) E_0 (resets)
+static int run_impl(mpgabor* h, const double* x_dev, int64_t Ls, int64_t maxit, double errdb, const double* etol_abs,
+                    mpg_atom* atoms_dev, double* energy_dev, double* coef_dev, mpg_result* res, void* stream) {
   if (!h) return MPG_EINVAL;
   if (!x_dev || !energy_dev || !res || (maxit > 0 && !atoms_dev)) return h->fail(MPG_EINVAL, "null pointer");
   if (Ls < 1) return h->fail(MPG_EINVAL, "Ls must be >= 1");
@@ -727,7 +729,7 @@ extern "C" int mpgabor_run(mpgabor* h, const double* x_dev, int64_t Ls, int64_t 
   TRY_CUDA(h, cudaStreamSynchronize(st));
   if (nonfinite) return h->fail(MPG_ENONFINITE, "x contains NaN or Inf");
   // stop level 10^(errdb/10) E_0
-  const double Etol = (errdb == -INFINITY) ? -INFINITY : std::pow(10.0, errdb / 10.0) * E0;
+  const double Etol = etol_abs ? *etol_abs : (errdb == -INFINITY) ? -INFINITY : std::pow(10.0, errdb / 10.0) * E0;
   P.dicts = h->d_geo.as<DictGeo>();
   P.own = h->d_own.as<OwnGeo>();
   P.pairs = h->d_pairs.as<PairGeo>();
@@ -781,6 +783,92 @@ extern "C" int mpgabor_run(mpgabor* h, const double* x_dev, int64_t Ls, int64_t 
   res->E0 = E0;
   res->E_final = lr.E_final;
   res->rounds = h->kind == 2 ? lr.rounds : lr.n_done + 1;
+  return MPG_OK;
+}
+
+extern "C" int mpgabor_run(mpgabor* h, const double* x_dev, int64_t Ls, int64_t maxit, double errdb,
+                           mpg_atom* atoms_dev, double* energy_dev, double* coef_dev, mpg_result* res,
+                           void* stream) {
+  return run_impl(h, x_dev, Ls, maxit, errdb, nullptr, atoms_dev, energy_dev, coef_dev, res, stream);
+}
+
+// Alg. 2: passes of the loop on the signal-domain residual r_out (zero-padded
+// to L, reading Z3), each started from c^ = D^* r_out (the DGT of run_impl) and stopped
+// after reset_every selections or by the inner stop rules, then r_out -= D c (synthesis
+// of the pass's atoms on all L samples).  The stop level stays 10^(errdb/10) ||x||^2.
+extern "C" int mpgabor_run_reset(mpgabor* h, const double* x_dev, int64_t Ls, int64_t maxit, double errdb,
+                                 int64_t reset_every, mpg_atom* atoms_dev, double* energy_dev, mpg_result* res,
+                                 void* stream) {
+  if (!h) return MPG_EINVAL;
+  if (!x_dev || !energy_dev || !res || (maxit > 0 && !atoms_dev)) return h->fail(MPG_EINVAL, "null pointer");
+  if (Ls < 1 || maxit < 0 || reset_every < 1) return h->fail(MPG_EINVAL, "need Ls >= 1, maxit >= 0, reset_every >= 1");
+  if (std::isnan(errdb)) return h->fail(MPG_EINVAL, "errdb is NaN");
+  if (!h->have_kernels) return h->fail(MPG_ESTATE, "mpgabor_kernels must run before mpgabor_run_reset");
+  int rc = enter_device(h);
+  if (rc) return rc;
+  rc = ensure_layout(h, Ls);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t L = h->L;
+  TRY_CUDA(h, h->rr.ensure(sizeof(double) * L));
+  TRY_CUDA(h, h->yy.ensure(sizeof(double) * L));
+  TRY_CUDA(h, cudaMemsetAsync(h->rr.p, 0, sizeof(double) * L, st));
+  TRY_CUDA(h, cudaMemcpyAsync(h->rr.p, x_dev, sizeof(double) * Ls, cudaMemcpyDeviceToDevice, st));
+  // ||x||^2 and the absolute stop level
+  TRY_CUDA(h, cudaMemsetAsync(h->flag.p, 0, sizeof(int), st));
+  TRY_LAUNCH(h, 2, launch_pad_energy(x_dev, Ls, h->xp.as<double>(), L, h->partial.as<double>(), h->flag.as<int>(),
+                                     h->E0.as<double>(), st));
+  double E0 = 0.0;
+  int nonfinite = 0;
+  TRY_CUDA(h, cudaMemcpyAsync(&E0, h->E0.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+  TRY_CUDA(h, cudaMemcpyAsync(&nonfinite, h->flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  TRY_CUDA(h, cudaStreamSynchronize(st));
+  if (nonfinite) return h->fail(MPG_ENONFINITE, "x contains NaN or Inf");
+  const double Etol = (errdb == -INFINITY) ? -INFINITY : std::pow(10.0, errdb / 10.0) * E0;
+  int64_t k = 0, rounds = 0;
+  int stop = MPG_STOP_MAXIT, passes = 0;
+  float t_loop = 0.f, t_dgt = 0.f;
+  while (k < maxit) {
+    mpg_result r{};
+    rc = run_impl(h, h->rr.as<double>(), L, std::min<int64_t>(reset_every, maxit - k), errdb, &Etol,
+                  atoms_dev + k, energy_dev + k, nullptr, &r, stream);
+    if (rc) return rc;
+    ++passes;
+    rounds += r.rounds;
+    t_loop += h->t_loop;
+    t_dgt += h->t_dgt;
+    if (r.n_atoms == 0) {  // the true residual energy reached the level, or a zero score
+      stop = r.stop_reason;
+      break;
+    }
+    rc = mpgabor_synth(h, atoms_dev + k, r.n_atoms, h->yy.as<double>(), L, stream);   // D c on all L samples
+    if (rc) return rc;
+    TRY_LAUNCH(h, 1, launch_sub(h->rr.as<double>(), h->yy.as<double>(), L, st));       // r_out -= D c
+    k += r.n_atoms;
+    if (r.stop_reason == MPG_STOP_ZERO) {
+      stop = MPG_STOP_ZERO;
+      break;
+    }
+  }
+  double Ek = E0;
+  TRY_CUDA(h, cudaMemcpyAsync(&Ek, energy_dev + k, sizeof(double), cudaMemcpyDeviceToHost, st));
+  TRY_CUDA(h, cudaStreamSynchronize(st));
+  h->t_loop = t_loop;
+  h->t_dgt = t_dgt;
+  h->passes = passes;
+  res->n_atoms = k;
+  res->L_pad = L;
+  res->stop_reason = stop;
+  res->cluster = h->lay_C;
+  res->E0 = E0;
+  res->E_final = Ek;
+  res->rounds = rounds;
+  return MPG_OK;
+}
+
+extern "C" int mpgabor_last_passes(const mpgabor* h, int32_t* passes) {
+  if (!h || !passes) return MPG_EINVAL;
+  *passes = h->passes;
   return MPG_OK;
 }
 

@@ -110,3 +110,16 @@ cudaError_t launch_synth_ola(const double* frames, const DictGeo& d, const doubl
   synth_ola_kernel<<<blocks, 256, 0, st>>>(frames, d.a, d.M, d.N, d.gl, g, L, L, y, accumulate);
   return cudaGetLastError();
 }
+
+// r -= y (Alg. 2 step 2c, r_out <- r_out - D c), grid-stride over n samples
+__global__ void sub_kernel(double* __restrict__ r, const double* __restrict__ y, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    r[i] -= y[i];
+}
+
+cudaError_t launch_sub(double* r, const double* y, int64_t n, cudaStream_t st) {
+  const int threads = 256;
+  const int64_t blocks = std::min<int64_t>((n + threads - 1) / threads, 148 * 8);
+  sub_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), threads, 0, st>>>(r, y, n);
+  return cudaGetLastError();
+}

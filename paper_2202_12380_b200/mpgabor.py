@@ -60,6 +60,9 @@ _SIGS = {
     "mpgabor_run": ([_P, _P, _I64, _I64, ctypes.c_double, _P, _P, _P, ctypes.POINTER(mpg_result), _P],
                     ctypes.c_int),
     "mpgabor_synth": ([_P, _P, _I64, _P, _I64, _P], ctypes.c_int),
+    "mpgabor_run_reset": ([_P, _P, _I64, _I64, ctypes.c_double, _I64, _P, _P, ctypes.POINTER(mpg_result), _P],
+                          ctypes.c_int),
+    "mpgabor_last_passes": ([_P, ctypes.POINTER(_I32)], ctypes.c_int),
     "mpgabor_decompose_host": ([_P, _P, _I64, _I64, ctypes.c_double, _P, _P, _P,
                                 ctypes.POINTER(mpg_result), _P], ctypes.c_int),
     "mpgabor_set_launch": ([_P, _I32, _I32, _I32, _I32], ctypes.c_int),
@@ -140,6 +143,19 @@ def mpgabor_run(h, x_dev, Ls, maxit, errdb, atoms_dev, energy_dev, coef_dev=None
     _check(h, _lib.mpgabor_run(h, _ptr(x_dev), int(Ls), int(maxit), float(errdb), _ptr(atoms_dev),
                                _ptr(energy_dev), _ptr(coef_dev), ctypes.byref(res), _stream(stream)))
     return res
+
+
+def mpgabor_run_reset(h, x_dev, Ls, maxit, errdb, reset_every, atoms_dev, energy_dev, stream=None):
+    res = mpg_result()
+    _check(h, _lib.mpgabor_run_reset(h, _ptr(x_dev), int(Ls), int(maxit), float(errdb), int(reset_every),
+                                     _ptr(atoms_dev), _ptr(energy_dev), ctypes.byref(res), _stream(stream)))
+    return res
+
+
+def mpgabor_last_passes(h):
+    n = _I32()
+    _check(h, _lib.mpgabor_last_passes(h, ctypes.byref(n)))
+    return n.value
 
 
 def mpgabor_synth(h, atoms_dev, n_atoms, y_dev, Ls, stream=None):
@@ -322,6 +338,23 @@ class MPGabor:
         en = energy[: n + 1].cpu().numpy()
         return RunOutput(at, en, res.stop_reason, res.E0, res.L_pad, res.cluster,
                          coef.view(torch.complex128) if coef is not None else None, atoms, res.rounds)
+
+    def run_reset(self, x, maxit, errdb=-math.inf, reset_every=1000, stream=None):
+        """Alg. 2 (resets); returns RunOutput (passes in .rounds is the loop rounds)."""
+        torch = self.torch
+        if not isinstance(x, torch.Tensor):
+            x = torch.as_tensor(np.ascontiguousarray(x, dtype=np.float64)).cuda()
+        assert x.dtype == torch.float64 and x.is_cuda and x.is_contiguous()
+        Ls = x.shape[0]
+        atoms, energy, _ = self.alloc(maxit, Ls)
+        res = mpgabor_run_reset(self.h, x, Ls, maxit, errdb, reset_every, atoms, energy, stream)
+        n = res.n_atoms
+        at = np.frombuffer(atoms[: n * ATOM_DTYPE.itemsize].cpu().numpy().tobytes(), dtype=ATOM_DTYPE)
+        en = energy[: n + 1].cpu().numpy()
+        return RunOutput(at, en, res.stop_reason, res.E0, res.L_pad, res.cluster, None, atoms, res.rounds)
+
+    def last_passes(self):
+        return mpgabor_last_passes(self.h)
 
     def synth(self, atoms_dev, n_atoms, Ls, stream=None):
         torch = self.torch

@@ -408,3 +408,60 @@ def test_planted_atoms_recovered_c0(mpg):
     found = {(int(a["m"]), int(a["n"])) for a in out.atoms[:40]}
     assert len(planted & found) >= 18
     mp.close()
+
+
+# ---------------------------------------------------------------------------
+# Alg. 2: approximate coefficient-domain MP with reset
+# ---------------------------------------------------------------------------
+RESET_CASES = [("C1", "f64", 4000, 500), ("C2", "f64", 3000, 1000), ("C1", "f32", 3000, 700)]
+
+
+@pytest.mark.parametrize("name,prec,K,every", RESET_CASES)
+def test_reset_matches_oracle(mpg, name, prec, K, every):
+    cfg = CONFIGS[name]
+    x, S = setup_of(name)
+    ref = oloop.mp_run_reset(x, cfg.dicts, cfg.thr, K, cfg.errdb, every, K=S.K)
+    mp = mpg.MPGabor(cfg.dicts, cfg.thr, prec)
+    out = mp.run_reset(torch.from_numpy(x).cuda(), K, cfg.errdb, every)
+    assert mp.last_passes() == ref.passes
+    lay = mp.layout(cfg.Ls)
+    idx = out.index(lay[3], lay[2])
+    if prec == "f64":
+        assert out.n == ref.n and out.stop == ref.stop
+        assert np.array_equal(idx, ref.index), f"first divergence at {first_divergence(idx, ref.index)}"
+        rel = np.abs(out.energy - ref.energy) / np.abs(ref.energy)
+        assert rel.max() <= FP64_E_TOL, rel.max()
+        # pass starts carry the true residual energy
+        np.testing.assert_allclose(out.energy[::every], ref.energy[::every], rtol=1e-10)
+    else:
+        d = first_divergence(idx, ref.index)
+        assert d >= min(out.n, ref.n) or d > 100
+        assert abs(out.energy[-1] - ref.energy[-1]) / S.E0 <= 1e-4
+    mp.close()
+
+
+def test_reset_threshold_zero_equals_signal_mp(mpg):
+    dicts = (Dict(HANN, 16, 4, 16), Dict(HANN, 8, 2, 8))
+    x = random_signal(96, 21)
+    mp = mpg.MPGabor(dicts, 0.0, "f64")
+    out = mp.run_reset(torch.from_numpy(x).cuda(), 60, -math.inf, 7)
+    at, e, _, _, _ = dense.signal_mp(x, dicts, 60)
+    S = oracle.Setup.build(x, dicts, 0.0)
+    off, MR = np.asarray(S.lay.off), np.asarray(S.lay.MR)
+    sidx = off[at["w"]] + at["n"].astype(np.int64) * MR[at["w"]] + at["m"]
+    lay = mp.layout(x.size)
+    assert np.array_equal(out.index(lay[3], lay[2]), sidx)
+    np.testing.assert_allclose(out.energy, e, rtol=0, atol=1e-11 * e[0])
+    mp.close()
+
+
+def test_reset_every_large_equals_run(mpg):
+    cfg = CONFIGS["C1"]
+    x, _ = setup_of("C1")
+    xd = torch.from_numpy(x).cuda()
+    mp = mpg.MPGabor(cfg.dicts, cfg.thr, "f64")
+    a = mp.run(xd, 2000, cfg.errdb)
+    b = mp.run_reset(xd, 2000, cfg.errdb, 10**9)
+    assert mp.last_passes() == 1
+    assert a.atoms.tobytes() == b.atoms.tobytes() and a.energy.tobytes() == b.energy.tobytes()
+    mp.close()
