@@ -148,6 +148,16 @@ int mpgabor_run_reset(mpgabor* h, const double* x_dev, int64_t Ls, int64_t maxit
                       void* cuda_stream);
 /* Number of passes of the last mpgabor_run_reset (host output). */
 int mpgabor_last_passes(const mpgabor* h, int32_t* passes);
+/* Batched independent signals: B >= 1 signals of Ls
+ * samples each, decomposed concurrently with the same dictionaries and kernels,
+ * one 16-CTA cluster per signal (~9 run at once on a B200's 148 SMs, the rest
+ * queue).  x_dev: device fp64[B][Ls]; atoms_dev: mpg_atom[B][maxit]; energy_dev:
+ * double[B][maxit+1]; res: host mpg_result[B].  Every signal's results equal those
+ * of mpgabor_run on it with the one-selection kernel (bit for bit).  Uses the
+ * one-selection cluster kernel regardless of mpgabor_set_batch.  Synchronises
+ * cuda_stream. */
+int mpgabor_run_batch(mpgabor* h, const double* x_dev, int32_t B, int64_t Ls, int64_t maxit, double errdb,
+                      mpg_atom* atoms_dev, double* energy_dev, mpg_result* res, void* cuda_stream);
 /* Synthesis of the approximation from an atom list (Eq. (18)):
  * y = sum_atoms c~ d (self-conjugate) or 2 Re(c~ d) (pairs), on L_pad samples,
  * truncated to Ls and written to y_dev (device fp64[Ls]).  atoms_dev: device

@@ -72,6 +72,11 @@ struct LoopParams {
   int floor_mode;                // 1: skip the update (latency-floor measurement; results invalid)
   void* gx_rec;                  // one-selection kernel, grid mode: Rec<R>[2][C] roots in global memory (else null)
   unsigned long long* gx_stamp;  // [2][C] iteration stamps of gx_rec (zeroed before the launch)
+  const double* E0v;             // batched signals (one-selection cluster kernel): per-slot E_0, stop level
+  const double* Etolv;           //   (null: the scalars E0 / Etol)
+  long long slot_grid;           //   grid elements per slot; the records per slot are C * Lc
+  long long slot_atoms;          //   atoms per slot (= maxit); energies per slot = slot_atoms + 1
+  int nslot;                     //   signals (clusters) of the launch
   int spec;                      // multi-selection: candidates per round (1..multi_max_batch())
   void* backup;                  // multi-selection: per-CTA tile backups [C][bk_cap][TW] (cplx<R>)
   long long bk_cap;              // items per CTA per round the backup holds

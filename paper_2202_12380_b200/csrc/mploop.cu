@@ -22,6 +22,7 @@
 //
 // Every coefficient is touched only by its tile's owner CTA, so the update needs
 // no atomics and no second cluster barrier.  The run is deterministic.
+#include <algorithm>
 #include <cooperative_groups.h>
 #include "loopcore.cuh"
 
@@ -131,9 +132,16 @@ __global__ void __launch_bounds__(512, 1) mp_loop_kernel(const LoopParams P) {
   int* stamp = reinterpret_cast<int*>(smem + L.stamp);
   int* list = reinterpret_cast<int*>(smem + L.list);
   int* cnt = reinterpret_cast<int*>(smem + L.cnt);
-  RecT* grec = reinterpret_cast<RecT*>(P.rec) + (long long)rank * P.Lc;
+  // batched independent signals: cluster `slot` works on signal `slot` (its own grids,
+  // records, atoms, energies and result; the kernels are shared)
+  const int slot = GX ? 0 : (int)(blockIdx.x / (unsigned)C);
+  const double E0s = P.E0v ? P.E0v[slot] : P.E0;
+  const double Etols = P.Etolv ? P.Etolv[slot] : P.Etol;
+  AtomOut* atoms_out = P.atoms + (long long)slot * P.slot_atoms;
+  double* energy_out = P.energy + (long long)slot * (P.slot_atoms + 1);
+  RecT* grec = reinterpret_cast<RecT*>(P.rec) + (long long)slot * C * P.Lc + (long long)rank * P.Lc;
   RecT* trec = SREC ? reinterpret_cast<RecT*>(smem + L.trec) : grec;
-  C2* grid = reinterpret_cast<C2*>(P.grid);
+  C2* grid = reinterpret_cast<C2*>(P.grid) + (long long)slot * P.slot_grid;
   const C2* kern = reinterpret_cast<const C2*>(P.kern);
 
   // ---- load tables -------------------------------------------------------
@@ -173,7 +181,7 @@ __global__ void __launch_bounds__(512, 1) mp_loop_kernel(const LoopParams P) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     mbar_arm(smem_addr(&mbar[0]), C * recbytes);
     mbar_arm(smem_addr(&mbar[1]), C * recbytes);
-    sel->E[0] = P.E0;
+    sel->E[0] = E0s;
     sel->stop = 0;
   }
   if constexpr (GX) __syncthreads();
@@ -201,7 +209,7 @@ __global__ void __launch_bounds__(512, 1) mp_loop_kernel(const LoopParams P) {
   if (warp == 0) publish_root(0);
   long long it = 0;
   int stop = 0;
-  const bool prof = P.prof != nullptr && rank == 0 && threadIdx.x == 0;
+  const bool prof = P.prof != nullptr && rank == 0 && slot == 0 && threadIdx.x == 0;
   long long ph[7] = {0, 0, 0, 0, 0, 0, 0};
 #define PROF_MARK(i)                \
   if (prof) {                        \
@@ -237,7 +245,7 @@ __global__ void __launch_bounds__(512, 1) mp_loop_kernel(const LoopParams P) {
       const double Ecur = sel->E[par];
       int st = 0;
       if (it >= P.maxit) st = 1;
-      else if (Ecur <= P.Etol) st = 2;
+      else if (Ecur <= Etols) st = 2;
       else if (Ecur < 0.0) st = 3;
       else if (!(best.s > (R)0)) st = 4;
       if (st) {
@@ -295,8 +303,8 @@ __global__ void __launch_bounds__(512, 1) mp_loop_kernel(const LoopParams P) {
               a.flags = selfc ? 1 : 0;
               a.re = tre;
               a.im = tim;
-              P.atoms[it] = a;
-              P.energy[it + 1] = En;
+              atoms_out[it] = a;
+              energy_out[it + 1] = En;
             }
           }
         } else {
@@ -467,9 +475,9 @@ __global__ void __launch_bounds__(512, 1) mp_loop_kernel(const LoopParams P) {
     PROF_MARK(6);
   }
   if (rank == 0 && threadIdx.x == 0) {
-    P.result->n_done = it;
-    P.result->stop = stop;
-    P.result->E_final = sel->E[it & 1];
+    P.result[slot].n_done = it;
+    P.result[slot].stop = stop;
+    P.result[slot].E_final = sel->E[it & 1];
   }
   if (prof) {
     for (int i = 0; i < 7; ++i) P.prof[i] = ph[i];
@@ -485,7 +493,7 @@ cudaError_t launch_t(const LoopParams& P, int threads, cudaStream_t st) {
   CUDA_OK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem_bytes));
   if (!GX && P.C > 8) CUDA_OK(cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(P.C, 1, 1);
+  cfg.gridDim = dim3(P.C * (GX ? 1 : std::max(1, P.nslot)), 1, 1);   // one cluster per signal
   cfg.blockDim = dim3(threads, 1, 1);
   cfg.dynamicSmemBytes = P.smem_bytes;
   cfg.stream = st;

@@ -77,6 +77,8 @@ struct mpgabor {
   int kind = 2;           // loop kernel: 0 mploop.cu, 2 mpmulti.cu
   bool force_single = false;  // multi-selection impossible for this layout: use mploop.cu
   bool gx = false;            // one-selection kernel as a cooperative grid (> 16 CTAs, global exchange)
+  bool batch_mode = false;    // batched signals: the one-selection cluster kernel, one cluster per signal
+  DevBuf etolv;               // batched signals: per-signal stop levels
   DevBuf gxrec, gxstamp;
 
   // per-length layout
@@ -199,7 +201,7 @@ extern "C" void mpgabor_destroy(mpgabor* h) {
     cudaSetDevice(h->device);
     for (DevBuf* b : {&h->tw, &h->roots, &h->win, &h->kern, &h->boxcopy, &h->d_pairs, &h->rho, &h->rho_meta,
                       &h->Hscratch, &h->mxbox, &h->d_geo, &h->grid, &h->rec, &h->xp, &h->partial, &h->flag,
-                      &h->E0, &h->result, &h->sol, &h->frames, &h->hx, &h->hatoms, &h->henergy, &h->hy, &h->prof, &h->d_own, &h->backup, &h->gxrec, &h->gxstamp, &h->rr, &h->yy})
+                      &h->E0, &h->result, &h->sol, &h->frames, &h->hx, &h->hatoms, &h->henergy, &h->hy, &h->prof, &h->d_own, &h->backup, &h->gxrec, &h->gxstamp, &h->rr, &h->yy, &h->etolv})
       b->release();
     for (auto e : h->ev)
       if (e) cudaEventDestroy(e);
@@ -589,10 +591,11 @@ static int ensure_layout(mpgabor* h, int64_t Ls) {
   // automatic grid mode: very wide updates (C4: ~54k coefficients per atom) spread over 64
   // CTAs beat one 16-CTA cluster despite the global-memory exchange
   const bool single = h->batch == 1 || (h->batch == 0 && !auto_multi(h));
-  const bool try_grid = h->cluster_req == 0 && single && mean_update(h) > 30000.0;
+  const bool try_grid = h->cluster_req == 0 && single && mean_update(h) > 30000.0 && !h->batch_mode;
+  if (h->batch_mode) h->force_single = true;
   const bool force_single0 = h->force_single;
   for (int pass = try_grid ? 0 : 1; pass < 2 && !ok; ++pass) {
-  const int creq = pass == 0 ? 64 : h->cluster_req;
+  const int creq = pass == 0 ? 64 : (h->batch_mode && h->cluster_req > MAX_CLUSTER ? 0 : h->cluster_req);
   h->gx = creq > MAX_CLUSTER;
   h->force_single = force_single0 || h->gx;  // grid mode: one-selection kernel
   for (int attempt = 0; attempt < 2 && !ok; ++attempt) {
@@ -683,53 +686,87 @@ extern "C" int mpgabor_launch_info(const mpgabor* h, int32_t* cluster, int32_t* 
 // run
 // ---------------------------------------------------------------------------
 // DGT + loop; etol_abs (nullable) replaces the stop level 10^(errdb/10) E_0 (resets)
+// B >= 1 independent signals of Ls samples (x_dev[B][Ls], atoms_dev[B][maxit],
+// energy_dev[B][maxit+1], res[B]): B > 1 runs the one-selection cluster kernel with one
+// cluster per signal (batched mode, no solution vector).
 static int run_impl(mpgabor* h, const double* x_dev, int64_t Ls, int64_t maxit, double errdb, const double* etol_abs,
-                    mpg_atom* atoms_dev, double* energy_dev, double* coef_dev, mpg_result* res, void* stream) {
+                    mpg_atom* atoms_dev, double* energy_dev, double* coef_dev, mpg_result* res, void* stream,
+                    int B = 1) {
   if (!h) return MPG_EINVAL;
   if (!x_dev || !energy_dev || !res || (maxit > 0 && !atoms_dev)) return h->fail(MPG_EINVAL, "null pointer");
   if (Ls < 1) return h->fail(MPG_EINVAL, "Ls must be >= 1");
   if (maxit < 0) return h->fail(MPG_EINVAL, "maxit must be >= 0");
   if (std::isnan(errdb)) return h->fail(MPG_EINVAL, "errdb is NaN");
   if (!h->have_kernels) return h->fail(MPG_ESTATE, "mpgabor_kernels must run before mpgabor_run");
+  if (B < 1 || (B > 1 && coef_dev)) return h->fail(MPG_EINVAL, "batched runs need B >= 1 and no solution vector");
   int rc = enter_device(h);
   if (rc) return rc;
+  if (h->batch_mode != (B > 1)) {  // batched signals: the one-selection cluster kernel (re-plan)
+    h->batch_mode = B > 1;
+    h->L = -1;
+  }
   rc = ensure_layout(h, Ls);
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   const int W = h->W;
+  LoopParams& P = h->lp;
+  if (B > 1) {
+    TRY_CUDA(h, h->grid.ensure(h->celem() * h->grid_elems * B));
+    TRY_CUDA(h, h->rec.ensure((h->f64() ? sizeof(Rec<double>) : sizeof(Rec<float>)) * P.C * P.Lc * B));
+  }
+  TRY_CUDA(h, h->E0.ensure(sizeof(double) * B));
+  TRY_CUDA(h, h->result.ensure(sizeof(LoopResult) * B));
+  TRY_CUDA(h, h->etolv.ensure(sizeof(double) * B));
+  const size_t recsz = h->f64() ? sizeof(Rec<double>) : sizeof(Rec<float>);
   TRY_CUDA(h, cudaEventRecord(h->ev[0], st));
   TRY_CUDA(h, cudaMemsetAsync(h->flag.p, 0, sizeof(int), st));
-  TRY_LAUNCH(h, 2, launch_pad_energy(x_dev, Ls, h->xp.as<double>(), h->L, h->partial.as<double>(), h->flag.as<int>(),
-                                h->E0.as<double>(), st));
-  for (int w = 0; w < W; ++w) {
-    const DictGeo& d = h->geo[w];
-    const double* g = h->win.as<double>() + h->win_off[w];
-    if (h->f64())
-      TRY_LAUNCH(h, 1, launch_dgt<double>(h->xp.as<double>(), h->L, d, g, h->tw.as<double2>(), h->twres,
-                                     h->grid.as<double2>() + d.grid_off, st));
-    else
-      TRY_LAUNCH(h, 1, launch_dgt<float>(h->xp.as<double>(), h->L, d, g, h->tw.as<double2>(), h->twres,
-                                    h->grid.as<float2>() + d.grid_off, st));
+  for (int b = 0; b < B; ++b) {
+    TRY_LAUNCH(h, 2, launch_pad_energy(x_dev + (int64_t)b * Ls, Ls, h->xp.as<double>(), h->L, h->partial.as<double>(),
+                                       h->flag.as<int>(), h->E0.as<double>() + b, st));
+    for (int w = 0; w < W; ++w) {
+      const DictGeo& d = h->geo[w];
+      const double* g = h->win.as<double>() + h->win_off[w];
+      const int64_t goff = d.grid_off + (int64_t)b * h->grid_elems;
+      if (h->f64())
+        TRY_LAUNCH(h, 1, launch_dgt<double>(h->xp.as<double>(), h->L, d, g, h->tw.as<double2>(), h->twres,
+                                            h->grid.as<double2>() + goff, st));
+      else
+        TRY_LAUNCH(h, 1, launch_dgt<float>(h->xp.as<double>(), h->L, d, g, h->tw.as<double2>(), h->twres,
+                                           h->grid.as<float2>() + goff, st));
+    }
   }
   TRY_CUDA(h, cudaEventRecord(h->ev[1], st));
-  LoopParams& P = h->lp;
-  if (h->f64())
-    TRY_LAUNCH(h, 2, launch_tile_init<double>(h->grid.as<double2>(), h->d_geo.as<DictGeo>(), h->d_own.as<OwnGeo>(), W, h->total_tiles, P.C, P.Lc,
-                                         h->TW, h->rec.as<Rec<double>>(), st));
-  else
-    TRY_LAUNCH(h, 2, launch_tile_init<float>(h->grid.as<float2>(), h->d_geo.as<DictGeo>(), h->d_own.as<OwnGeo>(), W, h->total_tiles, P.C, P.Lc,
-                                        h->TW, h->rec.as<Rec<float>>(), st));
+  for (int b = 0; b < B; ++b) {
+    unsigned char* recb = h->rec.as<unsigned char>() + recsz * P.C * P.Lc * b;
+    if (h->f64())
+      TRY_LAUNCH(h, 2, launch_tile_init<double>(h->grid.as<double2>() + (int64_t)b * h->grid_elems, h->d_geo.as<DictGeo>(),
+                                                h->d_own.as<OwnGeo>(), W, h->total_tiles, P.C, P.Lc, h->TW,
+                                                reinterpret_cast<Rec<double>*>(recb), st));
+    else
+      TRY_LAUNCH(h, 2, launch_tile_init<float>(h->grid.as<float2>() + (int64_t)b * h->grid_elems, h->d_geo.as<DictGeo>(),
+                                               h->d_own.as<OwnGeo>(), W, h->total_tiles, P.C, P.Lc, h->TW,
+                                               reinterpret_cast<Rec<float>*>(recb), st));
+    TRY_CUDA(h, cudaMemcpyAsync(energy_dev + (int64_t)b * (maxit + 1), h->E0.as<double>() + b, sizeof(double),
+                                cudaMemcpyDeviceToDevice, st));
+  }
   if (coef_dev) TRY_CUDA(h, cudaMemsetAsync(coef_dev, 0, sizeof(double2) * h->P_R, st));
-  TRY_CUDA(h, cudaMemcpyAsync(energy_dev, h->E0.p, sizeof(double), cudaMemcpyDeviceToDevice, st));
   TRY_CUDA(h, cudaEventRecord(h->ev[2], st));
-  double E0 = 0.0;
+  std::vector<double> E0s(B, 0.0), Etols(B, 0.0);
   int nonfinite = 0;
-  TRY_CUDA(h, cudaMemcpyAsync(&E0, h->E0.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+  TRY_CUDA(h, cudaMemcpyAsync(E0s.data(), h->E0.p, sizeof(double) * B, cudaMemcpyDeviceToHost, st));
   TRY_CUDA(h, cudaMemcpyAsync(&nonfinite, h->flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
   TRY_CUDA(h, cudaStreamSynchronize(st));
   if (nonfinite) return h->fail(MPG_ENONFINITE, "x contains NaN or Inf");
   // stop level 10^(errdb/10) E_0
-  const double Etol = etol_abs ? *etol_abs : (errdb == -INFINITY) ? -INFINITY : std::pow(10.0, errdb / 10.0) * E0;
+  for (int b = 0; b < B; ++b)
+    Etols[b] = etol_abs ? *etol_abs : (errdb == -INFINITY) ? -INFINITY : std::pow(10.0, errdb / 10.0) * E0s[b];
+  const double E0 = E0s[0], Etol = Etols[0];
+  TRY_CUDA(h, cudaMemcpyAsync(h->etolv.p, Etols.data(), sizeof(double) * B, cudaMemcpyHostToDevice, st));
+  P.nslot = B;
+  P.E0v = B > 1 ? h->E0.as<double>() : nullptr;
+  P.Etolv = B > 1 ? h->etolv.as<double>() : nullptr;
+  P.slot_grid = h->grid_elems;
+  P.slot_atoms = maxit;
   P.dicts = h->d_geo.as<DictGeo>();
   P.own = h->d_own.as<OwnGeo>();
   P.pairs = h->d_pairs.as<PairGeo>();
@@ -769,21 +806,32 @@ static int run_impl(mpgabor* h, const double* x_dev, int64_t Ls, int64_t maxit, 
   else
     TRY_LAUNCH(h, 1, launch_mp_loop(P, h->f64(), h->run_threads, st));
   TRY_CUDA(h, cudaEventRecord(h->ev[4], st));
-  LoopResult lr{};
-  TRY_CUDA(h, cudaMemcpyAsync(&lr, h->result.p, sizeof lr, cudaMemcpyDeviceToHost, st));
+  std::vector<LoopResult> lr(B);
+  TRY_CUDA(h, cudaMemcpyAsync(lr.data(), h->result.p, sizeof(LoopResult) * B, cudaMemcpyDeviceToHost, st));
   TRY_CUDA(h, cudaStreamSynchronize(st));
   TRY_CUDA(h, cudaEventElapsedTime(&h->t_dgt, h->ev[0], h->ev[1]));
   TRY_CUDA(h, cudaEventElapsedTime(&h->t_init, h->ev[1], h->ev[2]));
   TRY_CUDA(h, cudaEventElapsedTime(&h->t_loop, h->ev[3], h->ev[4]));
   if (P.prof) TRY_CUDA(h, cudaMemcpy(h->prof_host, P.prof, sizeof(long long) * 32, cudaMemcpyDeviceToHost));
-  res->n_atoms = lr.n_done;
-  res->L_pad = h->L;
-  res->stop_reason = lr.stop;
-  res->cluster = h->lay_C;
-  res->E0 = E0;
-  res->E_final = lr.E_final;
-  res->rounds = h->kind == 2 ? lr.rounds : lr.n_done + 1;
+  for (int b = 0; b < B; ++b) {
+    res[b].n_atoms = lr[b].n_done;
+    res[b].L_pad = h->L;
+    res[b].stop_reason = lr[b].stop;
+    res[b].cluster = h->lay_C;
+    res[b].E0 = E0s[b];
+    res[b].E_final = lr[b].E_final;
+    res[b].rounds = h->kind == 2 ? lr[b].rounds : lr[b].n_done + 1;
+  }
+  (void)E0;
+  (void)Etol;
   return MPG_OK;
+}
+
+extern "C" int mpgabor_run_batch(mpgabor* h, const double* x_dev, int32_t B, int64_t Ls, int64_t maxit, double errdb,
+                                 mpg_atom* atoms_dev, double* energy_dev, mpg_result* res, void* stream) {
+  if (!h) return MPG_EINVAL;
+  if (B < 1) return h->fail(MPG_EINVAL, "B must be >= 1");
+  return run_impl(h, x_dev, Ls, maxit, errdb, nullptr, atoms_dev, energy_dev, nullptr, res, stream, B);
 }
 
 extern "C" int mpgabor_run(mpgabor* h, const double* x_dev, int64_t Ls, int64_t maxit, double errdb,

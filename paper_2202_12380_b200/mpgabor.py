@@ -63,6 +63,8 @@ _SIGS = {
     "mpgabor_run_reset": ([_P, _P, _I64, _I64, ctypes.c_double, _I64, _P, _P, ctypes.POINTER(mpg_result), _P],
                           ctypes.c_int),
     "mpgabor_last_passes": ([_P, ctypes.POINTER(_I32)], ctypes.c_int),
+    "mpgabor_run_batch": ([_P, _P, _I32, _I64, _I64, ctypes.c_double, _P, _P, ctypes.POINTER(mpg_result), _P],
+                          ctypes.c_int),
     "mpgabor_decompose_host": ([_P, _P, _I64, _I64, ctypes.c_double, _P, _P, _P,
                                 ctypes.POINTER(mpg_result), _P], ctypes.c_int),
     "mpgabor_set_launch": ([_P, _I32, _I32, _I32, _I32], ctypes.c_int),
@@ -150,6 +152,13 @@ def mpgabor_run_reset(h, x_dev, Ls, maxit, errdb, reset_every, atoms_dev, energy
     _check(h, _lib.mpgabor_run_reset(h, _ptr(x_dev), int(Ls), int(maxit), float(errdb), int(reset_every),
                                      _ptr(atoms_dev), _ptr(energy_dev), ctypes.byref(res), _stream(stream)))
     return res
+
+
+def mpgabor_run_batch(h, x_dev, B, Ls, maxit, errdb, atoms_dev, energy_dev, stream=None):
+    res = (mpg_result * int(B))()
+    _check(h, _lib.mpgabor_run_batch(h, _ptr(x_dev), int(B), int(Ls), int(maxit), float(errdb), _ptr(atoms_dev),
+                                     _ptr(energy_dev), res, _stream(stream)))
+    return list(res)
 
 
 def mpgabor_last_passes(h):
@@ -352,6 +361,28 @@ class MPGabor:
         at = np.frombuffer(atoms[: n * ATOM_DTYPE.itemsize].cpu().numpy().tobytes(), dtype=ATOM_DTYPE)
         en = energy[: n + 1].cpu().numpy()
         return RunOutput(at, en, res.stop_reason, res.E0, res.L_pad, res.cluster, None, atoms, res.rounds)
+
+    def run_batch(self, X, maxit, errdb=-math.inf, stream=None):
+        """B independent signals X[B][Ls] (one cluster each); returns a list of RunOutput."""
+        torch = self.torch
+        if not isinstance(X, torch.Tensor):
+            X = torch.as_tensor(np.ascontiguousarray(X, dtype=np.float64)).cuda()
+        assert X.dtype == torch.float64 and X.is_cuda and X.is_contiguous() and X.dim() == 2
+        B, Ls = X.shape
+        atoms = torch.empty(B * max(int(maxit), 1) * ATOM_DTYPE.itemsize, dtype=torch.uint8, device="cuda")
+        energy = torch.empty(B * (int(maxit) + 1), dtype=torch.float64, device="cuda")
+        res = mpgabor_run_batch(self.h, X, B, Ls, maxit, errdb, atoms, energy, stream)
+        ab = atoms.cpu().numpy().tobytes()
+        en = energy.cpu().numpy()
+        outs = []
+        for b, r in enumerate(res):
+            n = r.n_atoms
+            a0 = b * int(maxit) * ATOM_DTYPE.itemsize
+            at = np.frombuffer(ab[a0: a0 + n * ATOM_DTYPE.itemsize], dtype=ATOM_DTYPE)
+            e0 = b * (int(maxit) + 1)
+            outs.append(RunOutput(at, en[e0: e0 + n + 1].copy(), r.stop_reason, r.E0, r.L_pad, r.cluster,
+                                  None, None, r.rounds))
+        return outs
 
     def last_passes(self):
         return mpgabor_last_passes(self.h)

@@ -216,11 +216,12 @@ _GENERATORS = {
 }
 
 
-def signal(cfg: Config | str) -> np.ndarray:
-    """The seeded fp64 input signal x (length Ls) of a config."""
+def signal(cfg: Config | str, seed: int | None = None) -> np.ndarray:
+    """The seeded fp64 input signal x (length Ls) of a config (``seed`` overrides the
+    config's seed: further signals of the same workload, e.g. for batched runs)."""
     if isinstance(cfg, str):
         cfg = CONFIGS[cfg]
-    return _GENERATORS[cfg.signal](cfg.seed, cfg.Ls)
+    return _GENERATORS[cfg.signal](cfg.seed if seed is None else seed, cfg.Ls)
 
 
 def random_signal(L: int, seed: int) -> np.ndarray:

@@ -465,3 +465,26 @@ def test_reset_every_large_equals_run(mpg):
     assert mp.last_passes() == 1
     assert a.atoms.tobytes() == b.atoms.tobytes() and a.energy.tobytes() == b.energy.tobytes()
     mp.close()
+
+
+# ---------------------------------------------------------------------------
+# batched independent signals: one cluster per signal
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("name,prec,B,K", [("C1", "f64", 4, 2000), ("C2", "f64", 10, 1500), ("C1", "f32", 3, 1500)])
+def test_batch_equals_individual_runs(mpg, name, prec, B, K):
+    cfg = CONFIGS[name]
+    X = np.stack([siggen.signal(cfg, seed=cfg.seed + 100 * b) for b in range(B)])
+    mp = mpg.MPGabor(cfg.dicts, cfg.thr, prec)
+    outs = mp.run_batch(torch.from_numpy(X).cuda(), K, cfg.errdb)
+    mp.set_batch(1)
+    for b in range(B):
+        one = mp.run(torch.from_numpy(X[b]).cuda(), K, cfg.errdb)
+        assert outs[b].n == one.n and outs[b].stop == one.stop
+        assert outs[b].atoms.tobytes() == one.atoms.tobytes(), b
+        assert outs[b].energy.tobytes() == one.energy.tobytes(), b
+    if prec == "f64":   # and the first signal against the oracle
+        S = oracle.Setup.build(X[0], cfg.dicts, cfg.thr)
+        ref = oloop.mp_run(S, K, cfg.errdb)
+        lay = mp.layout(cfg.Ls)
+        assert_fp64_parity(outs[0], outs[0].index(lay[3], lay[2]), ref)
+    mp.close()
