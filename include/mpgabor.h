@@ -150,8 +150,9 @@ int mpgabor_run_reset(mpgabor* h, const double* x_dev, int64_t Ls, int64_t maxit
 int mpgabor_last_passes(const mpgabor* h, int32_t* passes);
 /* Batched independent signals: B >= 1 signals of Ls
  * samples each, decomposed concurrently with the same dictionaries and kernels,
- * one 16-CTA cluster per signal (~9 run at once on a B200's 148 SMs, the rest
- * queue).  x_dev: device fp64[B][Ls]; atoms_dev: mpg_atom[B][maxit]; energy_dev:
+ * one cluster per signal (automatic cluster size 16 for B <= 4, 8 for B <= 12,
+ * else 4 CTAs, so that many signals run at once on the 148 SMs; mpgabor_set_launch
+ * overrides it; clusters that do not fit queue).  x_dev: device fp64[B][Ls]; atoms_dev: mpg_atom[B][maxit]; energy_dev:
  * double[B][maxit+1]; res: host mpg_result[B].  Every signal's results equal those
  * of mpgabor_run on it with the one-selection kernel (bit for bit).  Uses the
  * one-selection cluster kernel regardless of mpgabor_set_batch.  Synchronises

@@ -78,6 +78,7 @@ struct mpgabor {
   bool force_single = false;  // multi-selection impossible for this layout: use mploop.cu
   bool gx = false;            // one-selection kernel as a cooperative grid (> 16 CTAs, global exchange)
   bool batch_mode = false;    // batched signals: the one-selection cluster kernel, one cluster per signal
+  int batch_C = 16;           // batched signals: automatic cluster size per signal
   DevBuf etolv;               // batched signals: per-signal stop levels
   DevBuf gxrec, gxstamp;
 
@@ -595,7 +596,8 @@ static int ensure_layout(mpgabor* h, int64_t Ls) {
   if (h->batch_mode) h->force_single = true;
   const bool force_single0 = h->force_single;
   for (int pass = try_grid ? 0 : 1; pass < 2 && !ok; ++pass) {
-  const int creq = pass == 0 ? 64 : (h->batch_mode && h->cluster_req > MAX_CLUSTER ? 0 : h->cluster_req);
+  int creq = pass == 0 ? 64 : (h->batch_mode && h->cluster_req > MAX_CLUSTER ? 0 : h->cluster_req);
+  if (pass == 1 && h->batch_mode && h->cluster_req == 0) creq = h->batch_C;
   h->gx = creq > MAX_CLUSTER;
   h->force_single = force_single0 || h->gx;  // grid mode: one-selection kernel
   for (int attempt = 0; attempt < 2 && !ok; ++attempt) {
@@ -701,8 +703,12 @@ static int run_impl(mpgabor* h, const double* x_dev, int64_t Ls, int64_t maxit, 
   if (B < 1 || (B > 1 && coef_dev)) return h->fail(MPG_EINVAL, "batched runs need B >= 1 and no solution vector");
   int rc = enter_device(h);
   if (rc) return rc;
-  if (h->batch_mode != (B > 1)) {  // batched signals: the one-selection cluster kernel (re-plan)
+  // batched signals: the one-selection cluster kernel; smaller clusters let more signals
+  // run at once (measured aggregate it/s on B200, profiles/r01_batch.md)
+  const int bc = B <= 4 ? 16 : (B <= 12 ? 8 : 4);
+  if (h->batch_mode != (B > 1) || (B > 1 && bc != h->batch_C)) {
     h->batch_mode = B > 1;
+    h->batch_C = bc;
     h->L = -1;
   }
   rc = ensure_layout(h, Ls);
