@@ -184,6 +184,12 @@ int mpgabor_decompose_host(mpgabor* h, const double* x_host, int64_t Ls, int64_t
  * tile width 64, else 128, else global records).  Takes effect at the next run. */
 int mpgabor_set_launch(mpgabor* h, int32_t cluster, int32_t threads, int32_t tile_width, int32_t records);
 
+/* Selection rule (Alg. 1 step 1).  on = 0 (default): argmax |c^|^2 over the reduced
+ * coefficients (non-pedantic, reading Z9).  on = 1 ("pedantic"): argmax of
+ * the energy the selection removes, Eq. (20) with the Eq. (19) coefficient (|c~|^2
+ * -> (Re c^)^2 for self-conjugate atoms, 2|c^|^2 where <d, conj d> = 0).  Ties go to
+ * the lowest index either way.  EINVAL unless 0 or 1.  Takes effect at the next run. */
+int mpgabor_set_pedantic(mpgabor* h, int32_t on);
 /* Exact multi-selection: max_batch = the
  * most atoms one loop round may select and update at once.  Every round's extra
  * atoms are verified against the sequential argmax rule (Alg. 1, ties

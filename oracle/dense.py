@@ -184,3 +184,35 @@ def dense_alg1(x, dicts, thr, maxit, errdb=-math.inf):
         atoms.append((w, k, n, flags, ct.real, ct.imag))
         energy.append(E)
     return np.array(atoms, dtype=ATOM_DTYPE), np.array(energy), stop, c[red]
+
+
+def signal_mp_pedantic(x, dicts, maxit):
+    """Exact signal-domain MP with the pedantic selection rule, by brute
+    force: every step projects the residual onto span_R{Re d_p, Im d_p} (the real
+    atom pair d_p, conj d_p) for every reduced p by least squares on the materialised
+    atoms, selects the largest projection energy (ties -> lowest p) and subtracts the
+    projection.  Independent of Eqs. (19)/(20).  Returns (index[steps], energy[steps+1])."""
+    dicts = tuple(dicts)
+    lay = layout(dicts, x.size)
+    L = lay.L
+    _guard(L)
+    r = np.zeros(L)
+    r[: x.size] = x
+    D = dictionary(dicts, L)
+    bases = []
+    for p in range(D.shape[1]):
+        d = D[:, p]
+        B = np.stack([d.real, d.imag], axis=1) if np.linalg.norm(d.imag) > 1e-12 * np.linalg.norm(d.real) else d.real[:, None]
+        Q, _ = np.linalg.qr(B)
+        bases.append(Q)
+    idx, energy = [], [float(np.dot(r, r))]
+    for _ in range(maxit):
+        en = np.array([float(np.sum((Q.T @ r) ** 2)) for Q in bases])
+        p = int(np.argmax(en))
+        if not en[p] > 0:
+            break
+        Q = bases[p]
+        r = r - Q @ (Q.T @ r)
+        idx.append(p)
+        energy.append(float(np.dot(r, r)))
+    return np.asarray(idx, dtype=np.int64), np.asarray(energy)

@@ -57,7 +57,7 @@ def _load():
         _lib.orc_mp_run.restype = ctypes.c_int
         _lib.orc_mp_run.argtypes = [
             ctypes.c_int32, ctypes.POINTER(_Dict), ctypes.POINTER(_Kern), ctypes.c_void_p,
-            ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_double, ctypes.c_int32,
+            ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_double, ctypes.c_int32, ctypes.c_int32,
             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
             ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int32)]
     return _lib
@@ -90,8 +90,9 @@ def error_tolerance(errdb: float, E0: float) -> float:
 
 
 def mp_run(setup, maxit: int, errdb: float = -math.inf, full_scan: bool = False,
-           want_gaps: bool = True, etol: float | None = None) -> MpResult:
-    """Alg. 1 on the setup's grids; ``etol`` (absolute energy level) overrides errdb."""
+           want_gaps: bool = True, etol: float | None = None, pedantic: bool = False) -> MpResult:
+    """Alg. 1 on the setup's grids; ``etol`` (absolute energy level) overrides errdb;
+    ``pedantic`` selects by the Eq. (20) energy instead of |c^|^2."""
     lib = _load()
     lay = setup.lay
     W = len(setup.dicts)
@@ -110,6 +111,7 @@ def mp_run(setup, maxit: int, errdb: float = -math.inf, full_scan: bool = False,
     stop = ctypes.c_int32(0)
     rc = lib.orc_mp_run(W, dd, kk, res.ctypes.data, sol.ctypes.data, maxit,
                         error_tolerance(errdb, setup.E0) if etol is None else etol, setup.E0, int(full_scan),
+                        int(pedantic),
                         atoms.ctypes.data, energy.ctypes.data,
                         gaps.ctypes.data if want_gaps else None,
                         ctypes.byref(n_done), ctypes.byref(stop))

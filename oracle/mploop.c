@@ -53,11 +53,33 @@ typedef struct {
   double* fs; int64_t* fi;   /* per-frame best score / index */
   double* gs; int64_t* gi;   /* per-group best score / index */
   int64_t* touched; int64_t ntouched, cap;
+  int32_t pedantic;
 } st_t;
 
-static double score_at(const st_t* S, int64_t p) {
+static void rho_lookup(const st_t* S, int32_t u, int64_t k, double* rre, double* rim);
+
+/* selection score of coefficient p = atom (w, bin k):
+ *   non-pedantic (default, Z9): |c^|^2;
+ *   pedantic: the energy Eq. (20) removes, with c~ of Eq. (19) (reading Z11)
+ *   -- (Re c^)^2 for a self-conjugate atom (Z13), else 2[X^2+Y^2+Re rho(X^2-Y^2)-2 Im rho XY],
+ *   c~ = X + iY = (c^ - conj(rho) conj(c^)) * (1/(1-|rho|^2)), rho = h_ww(-2k, 0) (Z12). */
+static double score_wk(const st_t* S, int32_t w, int64_t k, int64_t p) {
   double re = S->res[2 * p], im = S->res[2 * p + 1];
-  return re * re + im * im;              /* |c^|^2, non-pedantic score (Z9) */
+  if (!S->pedantic) return re * re + im * im;
+  if (k == 0 || 2 * k == S->D[w].M) return re * re;
+  double rre, rim; rho_lookup(S, w, k, &rre, &rim);
+  double inv = 1.0 / (1.0 - (rre * rre + rim * rim));
+  double nre = re - (rre * re - rim * im);
+  double nim = im + (rre * im + rim * re);
+  double X = nre * inv, Y = nim * inv;
+  double X2 = X * X, Y2 = Y * Y, XY = X * Y;
+  return 2.0 * (X2 + Y2 + rre * (X2 - Y2) - 2.0 * rim * XY);
+}
+
+static double score_at(const st_t* S, int64_t p) {
+  int32_t w = 0;
+  while (w + 1 < S->W && S->D[w + 1].off <= p) ++w;
+  return score_wk(S, w, (p - S->D[w].off) % S->D[w].MR, p);
 }
 
 static void frame_wn(const st_t* S, int64_t f, int32_t* w, int64_t* n) {
@@ -72,7 +94,7 @@ static void scan_frame(st_t* S, int64_t f) {
   int64_t p0 = S->D[w].off + n * S->D[w].MR;
   double bs = -1.0; int64_t bi = p0;
   for (int64_t p = p0; p < p0 + S->D[w].MR; ++p) {
-    double s = score_at(S, p);
+    double s = score_wk(S, w, p - p0, p);
     if (s > bs) { bs = s; bi = p; }
   }
   S->fs[f] = bs; S->fi[f] = bi;
@@ -174,11 +196,11 @@ static void rho_lookup(const st_t* S, int32_t u, int64_t k, double* rre, double*
 }
 
 int orc_mp_run(int32_t W, const orc_dict* D, const orc_kernel* K, double* res, double* sol,
-               int64_t maxit, double Etol, double E0, int32_t full_scan,
+               int64_t maxit, double Etol, double E0, int32_t full_scan, int32_t pedantic,
                orc_atom* atoms, double* energy, double* gaps, int64_t* n_done, int32_t* stop) {
   st_t S;
   memset(&S, 0, sizeof S);
-  S.W = W; S.D = D; S.K = K; S.res = res;
+  S.W = W; S.D = D; S.K = K; S.res = res; S.pedantic = pedantic;
   S.fr_off = (int64_t*)malloc((size_t)(W + 1) * sizeof(int64_t));
   S.P = 0; S.F = 0;
   for (int32_t w = 0; w < W; ++w) { S.fr_off[w] = S.F; S.F += D[w].N; S.P += (int64_t)D[w].N * D[w].MR; }
@@ -199,7 +221,7 @@ int orc_mp_run(int32_t W, const orc_dict* D, const orc_kernel* K, double* res, d
     if (it >= maxit) { *stop = STOP_MAXIT; break; }
     if (E <= Etol) { *stop = STOP_ERRTOL; break; }
     if (E < 0.0) { *stop = STOP_NEGEST; break; }
-    /* b. selection p* = argmax |c^|^2, ties -> lowest p (Alg. 1 step 1, Z9/Z10) */
+    /* b. selection p* = argmax of the score (|c^|^2, or pedantic), ties -> lowest p (Alg. 1 step 1, Z9/Z10) */
     int64_t ps; double s1;
     if (full_scan) {
       s1 = -1.0; ps = 0;

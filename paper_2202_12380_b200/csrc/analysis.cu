@@ -6,6 +6,7 @@
 #include "launch.h"
 #include "fft.cuh"
 #include "argmax.cuh"
+#include "loopcore.cuh"
 
 // ---------------------------------------------------------------------------
 // windows: g(j), j = -floor(gl/2) .. ceil(gl/2)-1, unit norm
@@ -251,21 +252,10 @@ __global__ void kern_compact_kernel(const double2* __restrict__ H, int M_c, int 
 // N4 init: one warp per tile computes the tile record (best |c|^2, lowest index)
 // and stores it at rec[(g % C) * Lc + g / C] (CTA-major slices of the loop kernel).
 // ---------------------------------------------------------------------------
-template <typename R>
-__device__ __forceinline__ R score_of(R re, R im);
-template <>
-__device__ __forceinline__ double score_of<double>(double re, double im) {
-  return __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im));
-}
-template <>
-__device__ __forceinline__ float score_of<float>(float re, float im) {
-  return __fadd_rn(__fmul_rn(re, re), __fmul_rn(im, im));
-}
-
 template <typename R, int TW>
 __global__ void tile_init_kernel(const typename cplx<R>::t* __restrict__ grid, const DictGeo* __restrict__ dg,
                                  const OwnGeo* __restrict__ own, int W, int64_t total, int C, int64_t Lc,
-                                 Rec<R>* __restrict__ rec) {
+                                 Rec<R>* __restrict__ rec, SelScore sel) {
   // tile g of dictionary v, frame n goes to its owner CTA c = (frame_off_v + n) mod C,
   // local index loc_base(c,v) + ((n - n_first(c,v)) / C) * T_v + t (frame-major)
   const int lane = threadIdx.x & 31;
@@ -289,7 +279,10 @@ __global__ void tile_init_kernel(const typename cplx<R>::t* __restrict__ grid, c
         const int b = t * TW + ch * 32 + lane;
         if (b < d.MR) {
           const typename cplx<R>::t c = row[b];
-          const R s = score_of<R>(c.x, c.y);
+          // selection score (mpcore::sel_score: |c|^2, or the pedantic Eq. (20) energy)
+          const R s = sel.pedantic ? mpcore::sel_score<R>(c.x, c.y, b, d.M, true, sel.rho + sel.rho_meta[2 * W + v],
+                                                          sel.rho_meta[v], sel.rho_meta[W + v])
+                                   : mpcore::sel_score<R>(c.x, c.y, b, d.M, false, nullptr, 0, 0);
           const uint32_t p = (uint32_t)(d.off + n * d.MR + b);
           if (better(s, p, best.s, best.p)) {
             best.s = s;
@@ -406,14 +399,14 @@ template cudaError_t launch_kern_compact<float>(const double2*, int, int, double
 
 template <typename R>
 cudaError_t launch_tile_init(const typename cplx<R>::t* grid, const DictGeo* dg, const OwnGeo* own, int W,
-                             int64_t total, int C, int64_t Lc, int TW, Rec<R>* rec, cudaStream_t st) {
+                             int64_t total, int C, int64_t Lc, int TW, Rec<R>* rec, SelScore sel, cudaStream_t st) {
   const int64_t slots = (int64_t)C * Lc;
   rec_clear_kernel<R><<<(int)std::min<int64_t>(1184, (slots + 255) / 256), 256, 0, st>>>(rec, slots);
   const int blocks = (int)std::min<int64_t>(148 * 8, (total + 7) / 8);
   switch (TW) {
-    case 32: tile_init_kernel<R, 32><<<blocks, 256, 0, st>>>(grid, dg, own, W, total, C, Lc, rec); break;
-    case 64: tile_init_kernel<R, 64><<<blocks, 256, 0, st>>>(grid, dg, own, W, total, C, Lc, rec); break;
-    case 128: tile_init_kernel<R, 128><<<blocks, 256, 0, st>>>(grid, dg, own, W, total, C, Lc, rec); break;
+    case 32: tile_init_kernel<R, 32><<<blocks, 256, 0, st>>>(grid, dg, own, W, total, C, Lc, rec, sel); break;
+    case 64: tile_init_kernel<R, 64><<<blocks, 256, 0, st>>>(grid, dg, own, W, total, C, Lc, rec, sel); break;
+    case 128: tile_init_kernel<R, 128><<<blocks, 256, 0, st>>>(grid, dg, own, W, total, C, Lc, rec, sel); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
@@ -428,6 +421,6 @@ template cudaError_t launch_grid_export<double>(const double2*, const DictGeo*, 
 template cudaError_t launch_grid_export<float>(const float2*, const DictGeo*, int, int64_t, double2*, cudaStream_t);
 
 template cudaError_t launch_tile_init<double>(const double2*, const DictGeo*, const OwnGeo*, int, int64_t, int,
-                                              int64_t, int, Rec<double>*, cudaStream_t);
+                                              int64_t, int, Rec<double>*, SelScore, cudaStream_t);
 template cudaError_t launch_tile_init<float>(const float2*, const DictGeo*, const OwnGeo*, int, int64_t, int,
-                                             int64_t, int, Rec<float>*, cudaStream_t);
+                                             int64_t, int, Rec<float>*, SelScore, cudaStream_t);

@@ -17,9 +17,15 @@ template <typename R>
 cudaError_t launch_kern_compact(const double2* H, int M_c, int nu_first, double thr, const unsigned long long* mx,
                                 const PairGeo& pg, typename cplx<R>::t* kern, double2* boxcopy, RhoEnt* rho_row,
                                 cudaStream_t st);
+// sel: pedantic selection (rows of rho per dictionary: rho, rho_meta = {lo[W], n[W], off[W]}) or null
+struct SelScore {
+  int pedantic;
+  const RhoEnt* rho;
+  const int* rho_meta;
+};
 template <typename R>
 cudaError_t launch_tile_init(const typename cplx<R>::t* grid, const DictGeo* dg, const OwnGeo* own, int W,
-                             int64_t total, int C, int64_t Lc, int TW, Rec<R>* rec, cudaStream_t st);
+                             int64_t total, int C, int64_t Lc, int TW, Rec<R>* rec, SelScore sel, cudaStream_t st);
 
 template <typename R>
 cudaError_t launch_grid_export(const typename cplx<R>::t* grid, const DictGeo* dg, int W, int64_t P, double2* out,
@@ -77,6 +83,7 @@ struct LoopParams {
   long long slot_grid;           //   grid elements per slot; the records per slot are C * Lc
   long long slot_atoms;          //   atoms per slot (= maxit); energies per slot = slot_atoms + 1
   int nslot;                     //   signals (clusters) of the launch
+  int pedantic;                  // 1: select by the Eq. (20) energy (pedantic), else |c|^2
   int spec;                      // multi-selection: candidates per round (1..multi_max_batch())
   void* backup;                  // multi-selection: per-CTA tile backups [C][bk_cap][TW] (cplx<R>)
   long long bk_cap;              // items per CTA per round the backup holds

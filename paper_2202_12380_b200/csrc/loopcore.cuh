@@ -79,6 +79,34 @@ __device__ __forceinline__ C2 fold_update(C2 c, C2 z0, C2 hd, C2 hc, bool fd, bo
   return c;
 }
 
+// Selection score of coefficient c of atom (v, bin k) (Alg. 1 step 1).  Non-pedantic
+// (default, reading Z9): |c|^2.  Pedantic: the energy E~ that selecting the
+// atom removes, Eq. (20) with c~ of Eq. (19) -- c~ = Re c, E~ = c~^2 for a self-conjugate
+// atom (Z13); else rho = h_vv(-2k, 0) from the kept nu = 0 row (0 outside it, Z12),
+// c~ = (c - conj(rho) conj(c)) / (1 - |rho|^2) and E~ = 2 [X^2 + Y^2 + Re rho (X^2 - Y^2)
+// - 2 Im rho X Y]; with rho = 0 this is exactly 2 |c|^2.
+template <typename R>
+__device__ __forceinline__ R sel_score(R cre, R cim, int k, int M, bool pedantic, const RhoEnt* rho_row, int rho_lo,
+                                       int rho_n) {
+  using A = Ar<R>;
+  const R s2 = A::add(A::mul(cre, cre), A::mul(cim, cim));
+  if (!pedantic) return s2;
+  if (k == 0 || 2 * k == M) return A::mul(cre, cre);
+  int mu = (-2 * k) & (M - 1);
+  if (2 * mu > M) mu -= M;
+  const int ri = mu - rho_lo;
+  if (ri < 0 || ri >= rho_n) return A::add(s2, s2);
+  const RhoEnt rv = rho_row[ri];
+  const double cr = (double)cre, ci = (double)cim;
+  const double nre = __dsub_rn(cr, __dsub_rn(__dmul_rn(rv.re, cr), __dmul_rn(rv.im, ci)));
+  const double nim = __dadd_rn(ci, __dadd_rn(__dmul_rn(rv.re, ci), __dmul_rn(rv.im, cr)));
+  const double X = __dmul_rn(nre, rv.inv), Y = __dmul_rn(nim, rv.inv);
+  const double X2 = __dmul_rn(X, X), Y2 = __dmul_rn(Y, Y), XY = __dmul_rn(X, Y);
+  const double t = __dsub_rn(__dadd_rn(__dadd_rn(X2, Y2), __dmul_rn(rv.re, __dsub_rn(X2, Y2))),
+                             __dmul_rn(__dmul_rn(2.0, rv.im), XY));
+  return (R)__dmul_rn(2.0, t);
+}
+
 struct VGeo {           // update geometry for one target dictionary v, seen from this CTA
   long long kbase;      // first kernel entry of the alignment class
   int nr, nc;           // rows (frames) and columns (bins) of the class sub-box

@@ -394,7 +394,7 @@ __global__ void __launch_bounds__(512, 1) mp_loop_kernel(const LoopParams P) {
           const C2 c = fold_update<R>(cv[ch], z0, hd[ch], hc[ch], fd[ch], fc[ch], cfirst[ch]);
           if (bin < dv.MR) {
             if (fd[ch] || fc[ch]) row[bin] = c;
-            const R s = ScoreOps<R>::score(c.x, c.y);
+            const R s = sel_score<R>(c.x, c.y, bin, dv.M, P.pedantic, srho + rho_off[v], rho_lo[v], rho_n[v]);
             const uint32_t p = (uint32_t)dv.off + (uint32_t)nrow * (uint32_t)dv.MR + (uint32_t)bin;
             if (better(s, p, bs, bp)) {
               bs = s;

@@ -788,7 +788,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
             if (bin < MR) {
               const C2 c = cv[ch];
               row[bin] = c;
-              const R s = ScoreOps<R>::score(c.x, c.y);
+              const R s = sel_score<R>(c.x, c.y, bin, dv.M, P.pedantic, srho + rho_off[v], rho_lo[v], rho_n[v]);
               const uint32_t p = pbase + (uint32_t)bin;
               if (better(s, p, bs, bp)) {
                 bs = s;
@@ -858,7 +858,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
             const C2 c = fold_update<R>(cv[q][ch], z0, hd[q][ch], hc[q][ch], fd[q][ch], fc[q][ch], cf[q][ch]);
             if (bin < MR) {
               if (fd[q][ch] || fc[q][ch]) row[bin] = c;
-              const R s = ScoreOps<R>::score(c.x, c.y);
+              const R s = sel_score<R>(c.x, c.y, bin, dv.M, P.pedantic, srho + rho_off[v], rho_lo[v], rho_n[v]);
               const uint32_t p = pbase + (uint32_t)bin;
               if (better(s, p, bs, bp)) {
                 bs = s;

@@ -79,6 +79,7 @@ struct mpgabor {
   bool gx = false;            // one-selection kernel as a cooperative grid (> 16 CTAs, global exchange)
   bool batch_mode = false;    // batched signals: the one-selection cluster kernel, one cluster per signal
   int batch_C = 16;           // batched signals: automatic cluster size per signal
+  int pedantic = 0;           // 1: pedantic selection (Eq. (20) energies)
   DevBuf etolv;               // batched signals: per-signal stop levels
   DevBuf gxrec, gxstamp;
 
@@ -742,16 +743,17 @@ static int run_impl(mpgabor* h, const double* x_dev, int64_t Ls, int64_t maxit, 
     }
   }
   TRY_CUDA(h, cudaEventRecord(h->ev[1], st));
+  const SelScore sel{h->pedantic, h->rho.as<RhoEnt>(), h->rho_meta.as<int>()};
   for (int b = 0; b < B; ++b) {
     unsigned char* recb = h->rec.as<unsigned char>() + recsz * P.C * P.Lc * b;
     if (h->f64())
       TRY_LAUNCH(h, 2, launch_tile_init<double>(h->grid.as<double2>() + (int64_t)b * h->grid_elems, h->d_geo.as<DictGeo>(),
                                                 h->d_own.as<OwnGeo>(), W, h->total_tiles, P.C, P.Lc, h->TW,
-                                                reinterpret_cast<Rec<double>*>(recb), st));
+                                                reinterpret_cast<Rec<double>*>(recb), sel, st));
     else
       TRY_LAUNCH(h, 2, launch_tile_init<float>(h->grid.as<float2>() + (int64_t)b * h->grid_elems, h->d_geo.as<DictGeo>(),
                                                h->d_own.as<OwnGeo>(), W, h->total_tiles, P.C, P.Lc, h->TW,
-                                               reinterpret_cast<Rec<float>*>(recb), st));
+                                               reinterpret_cast<Rec<float>*>(recb), sel, st));
     TRY_CUDA(h, cudaMemcpyAsync(energy_dev + (int64_t)b * (maxit + 1), h->E0.as<double>() + b, sizeof(double),
                                 cudaMemcpyDeviceToDevice, st));
   }
@@ -792,6 +794,7 @@ static int run_impl(mpgabor* h, const double* x_dev, int64_t Ls, int64_t maxit, 
   P.sol = reinterpret_cast<double2*>(coef_dev);
   P.result = h->result.as<LoopResult>();
   P.floor_mode = (h->prof_mode & 2) ? 1 : 0;
+  P.pedantic = h->pedantic;
   P.prof = nullptr;
   if (h->prof_mode & 1) {
     TRY_CUDA(h, h->prof.ensure(sizeof(long long) * 32));
@@ -939,6 +942,13 @@ extern "C" int mpgabor_residual(mpgabor* h, double* out_dev, void* stream) {
     TRY_LAUNCH(h, 1, launch_grid_export<float>(h->grid.as<float2>(), h->d_geo.as<DictGeo>(), h->W, h->P_R,
                                           reinterpret_cast<double2*>(out_dev), st));
   TRY_CUDA(h, cudaStreamSynchronize(st));
+  return MPG_OK;
+}
+
+extern "C" int mpgabor_set_pedantic(mpgabor* h, int32_t on) {
+  if (!h) return MPG_EINVAL;
+  if (on != 0 && on != 1) return h->fail(MPG_EINVAL, "pedantic must be 0 or 1");
+  h->pedantic = on;
   return MPG_OK;
 }
 

@@ -69,6 +69,7 @@ _SIGS = {
                                 ctypes.POINTER(mpg_result), _P], ctypes.c_int),
     "mpgabor_set_launch": ([_P, _I32, _I32, _I32, _I32], ctypes.c_int),
     "mpgabor_set_batch": ([_P, _I32], ctypes.c_int),
+    "mpgabor_set_pedantic": ([_P, _I32], ctypes.c_int),
     "mpgabor_launch_info": ([_P, ctypes.POINTER(_I32), ctypes.POINTER(_I32), ctypes.POINTER(_I32),
                              ctypes.POINTER(_I32), ctypes.POINTER(_I64)], ctypes.c_int),
     "mpgabor_kernel_stats": ([_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I64)],
@@ -197,6 +198,10 @@ def mpgabor_set_batch(h, max_batch):
     _check(h, _lib.mpgabor_set_batch(h, int(max_batch)))
 
 
+def mpgabor_set_pedantic(h, on):
+    _check(h, _lib.mpgabor_set_pedantic(h, int(on)))
+
+
 def mpgabor_launch_info(h):
     c, t, tw, r = _I32(), _I32(), _I32(), _I32()
     sm = _I64()
@@ -321,6 +326,9 @@ class MPGabor:
 
     def set_batch(self, max_batch):
         mpgabor_set_batch(self.h, max_batch)
+
+    def set_pedantic(self, on):
+        mpgabor_set_pedantic(self.h, on)
 
     def alloc(self, maxit, Ls, want_coef=False):
         torch = self.torch

@@ -488,3 +488,49 @@ def test_batch_equals_individual_runs(mpg, name, prec, B, K):
         lay = mp.layout(cfg.Ls)
         assert_fp64_parity(outs[0], outs[0].index(lay[3], lay[2]), ref)
     mp.close()
+
+
+# ---------------------------------------------------------------------------
+# pedantic selection
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("batch", [1, 8])
+@pytest.mark.parametrize("name,K", [("C0", 500), ("C1", 10000), ("C2", 8000)])
+def test_pedantic_matches_oracle(mpg, name, K, batch):
+    cfg = CONFIGS[name]
+    x, S = setup_of(name)
+    ref = oloop.mp_run(S, K, cfg.errdb, pedantic=True)
+    mp = mpg.MPGabor(cfg.dicts, cfg.thr, "f64")
+    mp.set_pedantic(1)
+    mp.set_batch(batch)
+    out = mp.run(torch.from_numpy(x).cuda(), K, cfg.errdb)
+    lay = mp.layout(cfg.Ls)
+    assert_fp64_parity(out, out.index(lay[3], lay[2]), ref)
+    mp.close()
+
+
+def test_pedantic_tiny_equals_bruteforce(mpg):
+    dicts = (Dict(HANN, 16, 4, 16), Dict(HANN, 8, 2, 8))
+    x = random_signal(96, 23)
+    idx_ref, e_ref = dense.signal_mp_pedantic(x, dicts, 60)
+    mp = mpg.MPGabor(dicts, 0.0, "f64")
+    mp.set_pedantic(1)
+    out = mp.run(torch.from_numpy(x).cuda(), 60, -math.inf)
+    lay = mp.layout(x.size)
+    assert np.array_equal(out.index(lay[3], lay[2]), idx_ref)
+    np.testing.assert_allclose(out.energy, e_ref, rtol=0, atol=1e-11 * e_ref[0])
+    mp.close()
+
+
+def test_pedantic_fp32_and_batched(mpg):
+    cfg = CONFIGS["C2"]
+    x, S = setup_of("C2")
+    ref = oloop.mp_run(S, 4000, cfg.errdb, pedantic=True)
+    mp = mpg.MPGabor(cfg.dicts, cfg.thr, "f32")
+    mp.set_pedantic(1)
+    out = mp.run(torch.from_numpy(x).cuda(), 4000, cfg.errdb)
+    lay = mp.layout(cfg.Ls)
+    assert_fp32_parity(out, out.index(lay[3], lay[2]), ref, S.E0)
+    X = np.stack([x, siggen.signal(cfg, seed=cfg.seed + 100)])
+    outs = mp.run_batch(torch.from_numpy(X).cuda(), 4000, cfg.errdb)
+    assert outs[0].atoms.tobytes() == out.atoms.tobytes()
+    mp.close()

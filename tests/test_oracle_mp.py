@@ -231,3 +231,30 @@ def test_reset_recovers_truncation_drift():
     # the true energies at the pass starts decrease
     starts = reset.energy[::10][: reset.passes]
     assert np.all(np.diff(starts) < 0)
+
+
+# ---------------------------------------------------------------------------
+# pedantic selection: argmax of the energy the selection removes
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("dicts,L,steps", CASES[1:])
+def test_pedantic_threshold_zero_equals_bruteforce_projection_mp(dicts, L, steps):
+    # eps = 0: the pedantic coefficient-domain loop (Eq. (19)/(20) scores) equals MP that
+    # selects by the least-squares projection energy onto span{d, conj d} of materialised atoms
+    x = random_signal(L, 23)
+    S = oracle.Setup.build(x, dicts, 0.0)
+    r = loop.mp_run(S, steps, pedantic=True)
+    idx, e = dense.signal_mp_pedantic(x, dicts, steps)
+    assert np.array_equal(r.index, idx)
+    np.testing.assert_allclose(r.energy, e, rtol=0, atol=1e-11 * e[0])
+
+
+def test_pedantic_maxcache_equals_full_scan_and_differs_from_plain():
+    cfg = CONFIGS["C0"]
+    x = signal(cfg)
+    S = oracle.Setup.build(x, cfg.dicts, cfg.thr)
+    a = loop.mp_run(S, 300, cfg.errdb, pedantic=True)
+    b = loop.mp_run(S, 300, cfg.errdb, pedantic=True, full_scan=True)
+    c = loop.mp_run(S, 300, cfg.errdb)
+    assert np.array_equal(a.index, b.index) and np.array_equal(a.energy, b.energy)
+    assert not np.array_equal(a.index, c.index)          # the rule matters on C0 (low bins)
+    assert a.energy[-1] <= c.energy[-1]                   # and removes at least as much energy here
