@@ -35,6 +35,27 @@ __device__ __forceinline__ int warp_argmax(float s, uint32_t p, float& sbest, ui
   return __ffs(__ballot_sync(0xffffffffu, top && p == pbest)) - 1;
 }
 
+// Only the winning lane (score desc, index asc): one redux on the upper score word and a
+// ballot in the common case; the full comparison only when the upper words tie.
+__device__ __forceinline__ int warp_argmax_lane(double s, uint32_t p) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(s);
+  const unsigned hi = (unsigned)(b >> 32);
+  const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned m = __ballot_sync(0xffffffffu, hi == mhi);
+  if ((m & (m - 1)) == 0) return __ffs(m) - 1;
+  double sb;
+  uint32_t pb;
+  return warp_argmax(s, p, sb, pb);
+}
+__device__ __forceinline__ int warp_argmax_lane(float s, uint32_t p) {
+  const unsigned b = (unsigned)__float_as_int(s);
+  const unsigned mb = __reduce_max_sync(0xffffffffu, b);
+  const unsigned m = __ballot_sync(0xffffffffu, b == mb);
+  if ((m & (m - 1)) == 0) return __ffs(m) - 1;
+  const uint32_t pb = __reduce_min_sync(0xffffffffu, b == mb ? p : NO_INDEX);
+  return __ffs(__ballot_sync(0xffffffffu, b == mb && p == pb)) - 1;
+}
+
 // Full-record argmax: every lane ends with the winning record.
 template <typename R>
 __device__ __forceinline__ Rec<R> warp_best(const Rec<R>& r) {

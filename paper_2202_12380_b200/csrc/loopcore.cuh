@@ -107,6 +107,47 @@ __device__ __forceinline__ R sel_score(R cre, R cim, int k, int M, bool pedantic
   return (R)__dmul_rn(2.0, t);
 }
 
+// This lane's best (score desc, index asc) over its NCH bins bin0 + 32 ch of a tile row
+// (only bins < MR count); the pedantic test is taken once, outside the bin loop.
+template <typename R, typename C2, int NCH>
+__device__ __forceinline__ void lane_best(const C2 (&c)[NCH], int bin0, int MR, int M, uint32_t pbase, bool pedantic,
+                                          const RhoEnt* rho_row, int rho_lo, int rho_n, R& bs, uint32_t& bp, R& bre,
+                                          R& bim) {
+  bs = 0;
+  bp = NO_INDEX;
+  bre = 0;
+  bim = 0;
+  if (pedantic) {
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) {
+      const int bin = bin0 + ch * 32;
+      if (bin < MR) {
+        const R s = sel_score<R>(c[ch].x, c[ch].y, bin, M, true, rho_row, rho_lo, rho_n);
+        if (better(s, pbase + (uint32_t)bin, bs, bp)) {
+          bs = s;
+          bp = pbase + (uint32_t)bin;
+          bre = c[ch].x;
+          bim = c[ch].y;
+        }
+      }
+    }
+  } else {
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) {
+      const int bin = bin0 + ch * 32;
+      if (bin < MR) {
+        const R s = sel_score<R>(c[ch].x, c[ch].y, bin, M, false, nullptr, 0, 0);
+        if (better(s, pbase + (uint32_t)bin, bs, bp)) {
+          bs = s;
+          bp = pbase + (uint32_t)bin;
+          bre = c[ch].x;
+          bim = c[ch].y;
+        }
+      }
+    }
+  }
+}
+
 struct VGeo {           // update geometry for one target dictionary v, seen from this CTA
   long long kbase;      // first kernel entry of the alignment class
   int nr, nc;           // rows (frames) and columns (bins) of the class sub-box
@@ -215,10 +256,7 @@ template <typename R>
 __device__ __forceinline__ void warp_node(const Rec<R>* child, long long nchild, int node, Rec<R>* out, int lane) {
   const long long c = (long long)node * 32 + lane;
   const Rec<R> r = c < nchild ? child[c] : empty_rec(R(0));
-  R s;
-  uint32_t p;
-  const int wl = warp_argmax(r.s, r.p, s, p);
-  if (lane == wl) out[node] = r;
+  if (lane == warp_argmax_lane(r.s, r.p)) out[node] = r;
 }
 
 // 32-bit conservative key of a score for the multi-selection verification:

@@ -103,7 +103,8 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
 // distributed shared memory.  GX = true: a cooperative grid of C CTAs (C a power of
 // two up to 128, one per SM) exchanging roots through global memory (release/acquire
 // stamps); everything else is identical.
-template <typename R, int TW, bool SREC, bool GX>
+// PED: pedantic selection scores (compile-time, so the default path has no trace of it)
+template <typename R, int TW, bool SREC, bool GX, bool PED>
 __global__ void __launch_bounds__(512, 1) mp_loop_kernel(const LoopParams P) {
   using C2 = typename cplx<R>::t;
   using RecT = Rec<R>;
@@ -349,9 +350,10 @@ __global__ void __launch_bounds__(512, 1) mp_loop_kernel(const LoopParams P) {
         c.y += tim;
         *s = c;
       }
-      int v = 0;
+      // item ends of the target dictionaries in lanes v < W (items are v-major)
+      const int vend = lane < W ? vg[lane].base + vg[lane].nitems : 0x7fffffff;
       for (int gi = warp; gi < total; gi += NW) {
-        while (gi >= vg[v].base + vg[v].nitems) ++v;
+        const int v = __popc(__ballot_sync(0xffffffffu, gi >= vend));
         const VGeo& g = vg[v];
         const DictGeo& dv = sd[v];
         const PairGeo& pg = sp[u * W + v];
@@ -394,7 +396,7 @@ __global__ void __launch_bounds__(512, 1) mp_loop_kernel(const LoopParams P) {
           const C2 c = fold_update<R>(cv[ch], z0, hd[ch], hc[ch], fd[ch], fc[ch], cfirst[ch]);
           if (bin < dv.MR) {
             if (fd[ch] || fc[ch]) row[bin] = c;
-            const R s = sel_score<R>(c.x, c.y, bin, dv.M, P.pedantic, srho + rho_off[v], rho_lo[v], rho_n[v]);
+            const R s = sel_score<R>(c.x, c.y, bin, dv.M, PED, srho + rho_off[v], rho_lo[v], rho_n[v]);
             const uint32_t p = (uint32_t)dv.off + (uint32_t)nrow * (uint32_t)dv.MR + (uint32_t)bin;
             if (better(s, p, bs, bp)) {
               bs = s;
@@ -404,10 +406,7 @@ __global__ void __launch_bounds__(512, 1) mp_loop_kernel(const LoopParams P) {
             }
           }
         }
-        R ws;
-        uint32_t wp;
-        const int wl = warp_argmax(bs, bp, ws, wp);
-        if (lane == wl) {
+        if (lane == warp_argmax_lane(bs, bp)) {
           RecT rec;
           rec.s = bs;
           rec.re = bre;
@@ -430,10 +429,7 @@ __global__ void __launch_bounds__(512, 1) mp_loop_kernel(const LoopParams P) {
         const int node = list[idx];
         const long long c = (long long)node * 32 + lane;
         const RecT r = c < P.Lc ? trec[c] : empty_rec(R(0));
-        R s;
-        uint32_t p;
-        const int wl = warp_argmax(r.s, r.p, s, p);
-        if (lane == wl) {
+        if (lane == warp_argmax_lane(r.s, r.p)) {
           lev[node] = r;
           if (P.nlev > 1) {
             const int par2 = node >> 5;
@@ -453,10 +449,7 @@ __global__ void __launch_bounds__(512, 1) mp_loop_kernel(const LoopParams P) {
           const int node = list[P.lev_off[l] + idx];
           const int c = node * 32 + lane;
           const RecT r = c < P.lev_n[l - 1] ? lev[P.lev_off[l - 1] + c] : empty_rec(R(0));
-          R s;
-          uint32_t p;
-          const int wl = warp_argmax(r.s, r.p, s, p);
-          if (lane == wl) {
+          if (lane == warp_argmax_lane(r.s, r.p)) {
             lev[P.lev_off[l] + node] = r;
             if (l + 1 < P.nlev) {
               const int par2 = node >> 5;
@@ -489,7 +482,7 @@ __global__ void __launch_bounds__(512, 1) mp_loop_kernel(const LoopParams P) {
 
 template <typename R, int TW, bool SREC, bool GX>
 cudaError_t launch_t(const LoopParams& P, int threads, cudaStream_t st) {
-  auto kfn = mp_loop_kernel<R, TW, SREC, GX>;
+  auto kfn = P.pedantic ? mp_loop_kernel<R, TW, SREC, GX, true> : mp_loop_kernel<R, TW, SREC, GX, false>;
   CUDA_OK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem_bytes));
   if (!GX && P.C > 8) CUDA_OK(cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t cfg = {};
@@ -514,7 +507,7 @@ cudaError_t launch_t(const LoopParams& P, int threads, cudaStream_t st) {
 
 template <typename R, int TW, bool SREC>
 int max_cluster_t(int threads, size_t smem) {
-  auto kfn = mp_loop_kernel<R, TW, SREC, false>;
+  auto kfn = mp_loop_kernel<R, TW, SREC, false, false>;
   if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
       cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
     cudaGetLastError();
@@ -542,7 +535,7 @@ int max_cluster_t(int threads, size_t smem) {
 // co-resident CTAs of the global-exchange kernel (one per SM at most)
 template <typename R, int TW, bool SREC>
 int max_grid_t(int threads, size_t smem) {
-  auto kfn = mp_loop_kernel<R, TW, SREC, true>;
+  auto kfn = mp_loop_kernel<R, TW, SREC, true, false>;
   if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
     cudaGetLastError();
     return 0;

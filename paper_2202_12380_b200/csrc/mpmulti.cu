@@ -725,10 +725,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
     // ---- B. residual update (or roll-back) over this CTA's rows ------------
     // tile bookkeeping: record, candidate maximum, dirty level-0 node (no returns)
     auto finish = [&](int l, int g, R bs, uint32_t bp, R bre, R bim) {
-      R ws;
-      uint32_t wp;
-      const int wl = warp_argmax(bs, bp, ws, wp);
-      if (lane == wl) {
+      if (lane == warp_argmax_lane(bs, bp)) {
         RecT rec;
         rec.s = bs;
         rec.re = bre;
@@ -780,24 +777,15 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
             const int bin = t * TW + ch * 32 + lane;
             if (bin < MR) cv[ch] = bk[ch * 32 + lane];
           }
-          R bs = 0, bre = 0, bim = 0;
-          uint32_t bp = NO_INDEX;
 #pragma unroll
           for (int ch = 0; ch < NCH; ++ch) {
             const int bin = t * TW + ch * 32 + lane;
-            if (bin < MR) {
-              const C2 c = cv[ch];
-              row[bin] = c;
-              const R s = sel_score<R>(c.x, c.y, bin, dv.M, P.pedantic, srho + rho_off[v], rho_lo[v], rho_n[v]);
-              const uint32_t p = pbase + (uint32_t)bin;
-              if (better(s, p, bs, bp)) {
-                bs = s;
-                bp = p;
-                bre = c.x;
-                bim = c.y;
-              }
-            }
+            if (bin < MR) row[bin] = cv[ch];
           }
+          R bs, bre, bim;
+          uint32_t bp;
+          lane_best<R, C2, NCH>(cv, t * TW + lane, MR, dv.M, pbase, P.pedantic != 0, srho + rho_off[v], rho_lo[v],
+                                rho_n[v], bs, bp, bre, bim);
           finish(l0 + t, g, bs, bp, bre, bim);
         }
       } else {
@@ -845,8 +833,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
         for (int q = 0; q < 2; ++q) {
           if (tt + q >= Tr) break;
           const int t = t0 + tt + q;
-          R bs = 0, bre = 0, bim = 0;
-          uint32_t bp = NO_INDEX;
+          C2 cn[NCH];
 #pragma unroll
           for (int ch = 0; ch < NCH; ++ch) {
             const int bin = t * TW + ch * 32 + lane;
@@ -855,19 +842,13 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
               atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 17, (unsigned long long)(tn - ta));
               ta = tn;
             }
-            const C2 c = fold_update<R>(cv[q][ch], z0, hd[q][ch], hc[q][ch], fd[q][ch], fc[q][ch], cf[q][ch]);
-            if (bin < MR) {
-              if (fd[q][ch] || fc[q][ch]) row[bin] = c;
-              const R s = sel_score<R>(c.x, c.y, bin, dv.M, P.pedantic, srho + rho_off[v], rho_lo[v], rho_n[v]);
-              const uint32_t p = pbase + (uint32_t)bin;
-              if (better(s, p, bs, bp)) {
-                bs = s;
-                bp = p;
-                bre = c.x;
-                bim = c.y;
-              }
-            }
+            cn[ch] = fold_update<R>(cv[q][ch], z0, hd[q][ch], hc[q][ch], fd[q][ch], fc[q][ch], cf[q][ch]);
+            if (bin < MR && (fd[q][ch] || fc[q][ch])) row[bin] = cn[ch];
           }
+          R bs, bre, bim;
+          uint32_t bp;
+          lane_best<R, C2, NCH>(cn, t * TW + lane, MR, dv.M, pbase, P.pedantic != 0, srho + rho_off[v], rho_lo[v],
+                                rho_n[v], bs, bp, bre, bim);
           finish(l0 + t, g, bs, bp, bre, bim);
         }
         if (prof) {
@@ -903,10 +884,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
           const int node = (w0 + src) * 32 + __ffs(wd) - 1;
           const long long c = (long long)node * 32 + lane;
           const RecT rc = c < P.Lc ? trec[c] : empty_rec(R(0));
-          R s;
-          uint32_t p;
-          const int wl = warp_argmax(rc.s, rc.p, s, p);
-          if (lane == wl) {
+          if (lane == warp_argmax_lane(rc.s, rc.p)) {
             lev[node] = rc;
             if (P.nlev > 1) atomicOr(&dirty[dw_off[1] + (node >> 10)], 1u << ((node >> 5) & 31));
           }
@@ -927,10 +905,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
             const int node = (w0 - dw_off[l]) * 32 + b;
             const int c = node * 32 + lane;
             const RecT rc = c < P.lev_n[l - 1] ? lev[P.lev_off[l - 1] + c] : empty_rec(R(0));
-            R s;
-            uint32_t p;
-            const int wl = warp_argmax(rc.s, rc.p, s, p);
-            if (lane == wl) {
+            if (lane == warp_argmax_lane(rc.s, rc.p)) {
               lev[P.lev_off[l] + node] = rc;
               if (l + 1 < P.nlev) atomicOr(&dirty[dw_off[l + 1] + (node >> 10)], 1u << ((node >> 5) & 31));
             }

@@ -86,6 +86,8 @@ _SIGS = {
     "mpgabor_last_error": ([_P], ctypes.c_char_p),
 }
 for _name, (_args, _res) in _SIGS.items():
+    if os.environ.get("MPGABOR_LIB") and not hasattr(_lib, _name):
+        continue  # A/B timing of an older build: calls it lacks are unavailable
     _f = getattr(_lib, _name)
     _f.argtypes = _args
     _f.restype = _res
