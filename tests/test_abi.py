@@ -89,6 +89,23 @@ def test_precision_and_state_errors(mpg):
             assert "EINVAL" in str(e.value)
         for ok in (0, 1, 4, 8):
             mpg.mpgabor_set_batch(h, ok)
+        for bad in (-1, 2):
+            with pytest.raises(mpg.MpgError) as e:
+                mpg.mpgabor_set_pedantic(h, bad)
+            assert "EINVAL" in str(e.value)
+        mpg.mpgabor_set_pedantic(h, 1)
+        mpg.mpgabor_set_pedantic(h, 0)
+        for bad in (256, 48, 24):
+            with pytest.raises(mpg.MpgError):
+                mpg.mpgabor_set_launch(h, bad, 0, 0, 0)
+        for ok in (32, 64, 128):
+            mpg.mpgabor_set_launch(h, ok, 0, 0, 0)   # grid mode of the one-selection loop
+        dummy = ctypes.c_void_p(16)
+        res = mpg.mpg_result()
+        rc = mpg._lib.mpgabor_run_batch(h, dummy, 0, 1024, 10, -1.0, dummy, dummy, ctypes.byref(res), None)
+        assert mpg.ERRORS[rc] == "EINVAL"
+        rc = mpg._lib.mpgabor_run_reset(h, dummy, 1024, 10, -1.0, 0, dummy, dummy, ctypes.byref(res), None)
+        assert mpg.ERRORS[rc] == "EINVAL"                 # reset_every < 1
         with pytest.raises(mpg.MpgError) as e:
             mpg.mpgabor_kernel_stats(h)             # before mpgabor_kernels
         assert "ESTATE" in str(e.value)
