@@ -441,9 +441,31 @@ __global__ void __launch_bounds__(512, 1) mp_loop_kernel(const LoopParams P) {
     }
     __syncthreads();
     PROF_MARK(5);
+    // ---- D. upper node levels.  Grid mode (GX, the very large grids with nlev > 1):
+    //      one level at a time, the dirty nodes spread over the warps; one cluster:
+    //      warp 0 alone (measured faster there)
+    if constexpr (GX) {
+      for (int l = 1; l < P.nlev; ++l) {
+        const int nl = cnt[l];
+        for (int idx = warp; idx < nl; idx += NW) {
+          const int node = list[P.lev_off[l] + idx];
+          const int c = node * 32 + lane;
+          const RecT r = c < P.lev_n[l - 1] ? lev[P.lev_off[l - 1] + c] : empty_rec(R(0));
+          if (lane == warp_argmax_lane(r.s, r.p)) {
+            lev[P.lev_off[l] + node] = r;
+            if (l + 1 < P.nlev) {
+              const int par2 = node >> 5;
+              int* st2 = stamp + P.lev_off[l + 1];
+              if (atomicExch(&st2[par2], stampv) != stampv) list[P.lev_off[l + 1] + atomicAdd(&cnt[l + 1], 1)] = par2;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
     // ---- D. upper levels, top scan, publish root (warp 0) ------------------
     if (warp == 0) {
-      for (int l = 1; l < P.nlev; ++l) {
+      for (int l = 1; l < (GX ? 1 : P.nlev); ++l) {
         const int nl = cnt[l];
         for (int idx = 0; idx < nl; ++idx) {
           const int node = list[P.lev_off[l] + idx];
