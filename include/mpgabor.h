@@ -195,7 +195,7 @@ int mpgabor_set_pedantic(mpgabor* h, int32_t on);
  * atoms are verified against the sequential argmax rule (Alg. 1, ties
  * Z10) and rolled back bit-exactly when the proof fails, so the atom sequence,
  * coefficients and energies are those of the one-selection loop for every value.
- * 0 = automatic: batch 8 when the mean update of an atom is small (< 1500
+ * 0 = automatic: batch 8 when the mean update of an atom is small (< 3000
  * coefficients, estimated from the kernel boxes, and < 0.5 % of the reduced
  * coefficients), else one selection per
  * iteration (DESIGN.md §8 has the measured crossover); 1 = one selection per

@@ -216,6 +216,14 @@ __device__ __forceinline__ int vgeo(const PairGeo& pg, const DictGeo& du, const 
   return nitems;
 }
 
+// ---- named CTA barriers (id 0 is __syncthreads) ----
+__device__ __forceinline__ void bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(int id, int nthreads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
 // ---- cluster mailbox: st.async into remote shared memory + mbarrier complete_tx ----
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ uint32_t mapa(uint32_t a, int rank) {

@@ -56,13 +56,7 @@ template <typename R, int K>
 struct Msg {              // published by every CTA to every CTA at the end of a round
   Rec<R> list[K];         // its K best tile records, (score desc, index asc)
   uint32_t vkey[BMAX];    // per candidate: max score key over the candidate's tiles owned by the CTA
-  uint2 rect[K * 16];     // packed tiles(list[i]) in target dictionary v at [i * W + v] (W <= 16);
-                          // only the first K * W entries are pushed
 };
-template <typename R, int K>
-__host__ __device__ constexpr size_t msg_head() {
-  return sizeof(Rec<R>) * K + sizeof(uint32_t) * BMAX;
-}
 
 struct Ent {              // one merged list entry of the walk window
   double tre, tim, Et;    // c~ (Eq. (19)) and E~ (Eq. (20)) if selected
@@ -82,23 +76,19 @@ struct St {               // round state (shared memory)
   int mode;               // 0 select, 1 roll back candidates rb_from..G-1
   int rb_from;
   int stop;
+  int pick[BMAX];         // walk-window position of candidate g (its egeo row)
   uint32_t ckey[BMAX];    // score key of candidate g
   alignas(16) int ibase[BMAX * 16 + 4];  // this CTA's items (tile pairs) before (g, v), index g * 16 + v
   alignas(16) int tbase[BMAX * 16 + 4];  // this CTA's tiles (backup slots) before (g, v)
 };
 
 struct Smem {
-  size_t mbar, mail, mymsg, trec, lev, ent, egeo, wmask, st, vkey, sorted, tk, dwoff, dirty, pairs, dicts, own, roots,
+  size_t mbar, mail, mymsg, trec, lev, ent, egeo, wmask, rect, st, vkey, sorted, tk, stamp, list, cnt, pairs, dicts, own, roots,
       rho, rho_meta, total;
 };
 
 __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-__host__ __device__ inline int dirty_words(const LoopParams& P) {
-  int w = 0;
-  for (int l = 0; l < P.nlev; ++l) w += (P.lev_n[l] + 31) / 32;
-  return w;
-}
 
 __host__ __device__ inline Smem smem_layout(const LoopParams& P, size_t recsz, size_t msgsz) {
   Smem s;
@@ -117,13 +107,16 @@ __host__ __device__ inline Smem smem_layout(const LoopParams& P, size_t recsz, s
   o += (size_t)levtot * recsz;
   o = align_up(o, 16);
   s.ent = o;
-  o += sizeof(Ent) * BMAX;
+  o += sizeof(Ent) * NE;
   o = align_up(o, 16);
   s.egeo = o;
-  o += sizeof(VGeo) * BMAX * P.W;
+  o += sizeof(VGeo) * NE * P.W;
   o = align_up(o, 16);
   s.wmask = o;
   o += sizeof(uint32_t) * 2 * NE;
+  o = align_up(o, 16);
+  s.rect = o;
+  o += sizeof(uint2) * NE * P.W;
   o = align_up(o, 16);
   s.st = o;
   o += sizeof(St);
@@ -134,11 +127,12 @@ __host__ __device__ inline Smem smem_layout(const LoopParams& P, size_t recsz, s
   o += sizeof(int) * NE;
   s.tk = o;
   o += sizeof(int) * 64;
-  s.dwoff = o;
-  o += sizeof(int) * (MAX_LEVELS + 1);
-  o = align_up(o, 16);
-  s.dirty = o;
-  o += sizeof(uint32_t) * dirty_words(P);
+  s.stamp = o;
+  o += sizeof(int) * levtot;
+  s.list = o;
+  o += sizeof(int) * levtot;
+  s.cnt = o;
+  o += sizeof(int) * MAX_LEVELS;
   o = align_up(o, 16);
   s.pairs = o;
   o += sizeof(PairGeo) * P.W * P.W;
@@ -195,7 +189,7 @@ __device__ __forceinline__ void warp_pop_k(uint64_t key, uint32_t p, int id, int
 // holds the chunk winners.  Needs a barrier before; ends with one.
 template <typename R, int K>
 __device__ __forceinline__ void cta_topk(const LoopParams& P, const Rec<R>* lev, const Rec<R>* trec, int* tk,
-                                         int lane, int warp) {
+                                         int lane, int warp, int NW) {
   static_assert(K * 8 <= 32, "the merge holds 8 chunks x K winners in one warp");
   int* part = tk + 16;
   const int top = P.nlev - 1;
@@ -204,8 +198,8 @@ __device__ __forceinline__ void cta_topk(const LoopParams& P, const Rec<R>* lev,
     const int count = l >= 0 ? P.lev_n[l] : (int)P.Lc;
     const Rec<R>* arr = l >= 0 ? lev + P.lev_off[l] : trec;
     const int nq = first ? (count + 31) >> 5 : K;
-    if (warp < nq) {
-      int id = first ? warp * 32 + lane : (tk[warp] >= 0 ? tk[warp] * 32 + lane : -1);
+    for (int q = warp; q < nq; q += NW) {  // chunk q (fewer warps than chunks: several each)
+      int id = first ? q * 32 + lane : (tk[q] >= 0 ? tk[q] * 32 + lane : -1);
       uint64_t key = 0;
       uint32_t p = NO_INDEX;
       if (id >= 0 && id < count) {
@@ -214,7 +208,7 @@ __device__ __forceinline__ void cta_topk(const LoopParams& P, const Rec<R>* lev,
       } else {
         id = -1;
       }
-      warp_pop_k<K>(key, p, id, part + warp * K, lane);
+      warp_pop_k<K>(key, p, id, part + q * K, lane);
     }
     __syncthreads();
     if (warp == 0) {
@@ -287,11 +281,14 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
   VGeo* egeo = reinterpret_cast<VGeo*>(smem + L.egeo);
   uint32_t* wmeet = reinterpret_cast<uint32_t*>(smem + L.wmask);
   uint32_t* wcover = wmeet + NE;
+  uint2* rect = reinterpret_cast<uint2*>(smem + L.rect);
   St* st = reinterpret_cast<St*>(smem + L.st);
   uint32_t* vkey = reinterpret_cast<uint32_t*>(smem + L.vkey);
   int* sorted = reinterpret_cast<int*>(smem + L.sorted);
   int* tk = reinterpret_cast<int*>(smem + L.tk);
-  uint32_t* dirty = reinterpret_cast<uint32_t*>(smem + L.dirty);
+  int* stamp = reinterpret_cast<int*>(smem + L.stamp);   // dirty-node stamps and lists per level
+  int* list = reinterpret_cast<int*>(smem + L.list);
+  int* cnt = reinterpret_cast<int*>(smem + L.cnt);
   PairGeo* sp = reinterpret_cast<PairGeo*>(smem + L.pairs);
   DictGeo* sd = reinterpret_cast<DictGeo*>(smem + L.dicts);
   OwnGeo* sown = reinterpret_cast<OwnGeo*>(smem + L.own);
@@ -305,12 +302,6 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
   C2* grid = reinterpret_cast<C2*>(P.grid);
   const C2* kern = reinterpret_cast<const C2*>(P.kern);
   C2* backup = reinterpret_cast<C2*>(P.backup) + (long long)rank * P.bk_cap * TW;
-  int* dw_off = reinterpret_cast<int*>(smem + L.dwoff);  // first dirty word of each level
-  if (tid == 0) {
-    dw_off[0] = 0;
-    for (int l = 0; l < MAX_LEVELS; ++l) dw_off[l + 1] = dw_off[l] + (l < P.nlev ? (P.lev_n[l] + 31) / 32 : 0);
-  }
-  __syncthreads();
 
   // ---- load tables -------------------------------------------------------
   for (int i = tid; i < W * W; i += blockDim.x) sp[i] = P.pairs[i];
@@ -324,7 +315,12 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
   if (P.Rmax <= 4096)
     for (int i = tid; i < P.Rmax; i += blockDim.x) reinterpret_cast<double2*>(smem + L.roots)[i] = P.roots[i];
   for (int i = tid; i < P.rho_total; i += blockDim.x) srho[i] = P.rho[i];
-  for (int i = tid; i < dw_off[P.nlev]; i += blockDim.x) dirty[i] = 0;
+  {
+    int levtot = 0;
+    for (int l = 0; l < P.nlev; ++l) levtot += P.lev_n[l];
+    for (int i = tid; i < levtot; i += blockDim.x) stamp[i] = 0;
+  }
+  if (tid < MAX_LEVELS) cnt[tid] = 0;
   if (tid < BMAX) vkey[tid] = 0;
   if (SREC)
     for (long long i = tid; i < P.Lc; i += blockDim.x) trec[i] = grec[i];
@@ -338,7 +334,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
       warp_node(lev + P.lev_off[l - 1], (long long)P.lev_n[l - 1], i, lev + P.lev_off[l], lane);
     __syncthreads();
   }
-  const uint32_t msgbytes = (uint32_t)align_up(msg_head<R, K>() + sizeof(uint2) * K * W, 16);
+  const uint32_t msgbytes = (uint32_t)sizeof(MsgT);
   if (tid == 0) {
     mbar_init(smem_addr(&mbar[0]), 1);
     mbar_init(smem_addr(&mbar[1]), 1);
@@ -371,20 +367,6 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
       mymsg->vkey[lane] = vkey[lane];
       vkey[lane] = 0;
     }
-    // tiles(list[i]) in every target dictionary (CTA-independent part of Alg. 3's sets)
-    for (int t = lane; t < K * W; t += 32) {
-      const int i = t / W, v = t - i * W;
-      uint2 rc = make_uint2(0u, 0u);
-      if (tk[i] >= 0) {
-        const uint32_t p = trec[tk[i]].p;
-        int u, k, j;
-        decode_p(p, sd, W, u, k, j);
-        VGeo gg;
-        vgeo<LGTW>(sp[u * W + v], sd[u], sd[v], k, j, 0, C, lgC, gg);
-        rc = pack_rect(gg);
-      }
-      mymsg->rect[t] = rc;
-    }
     __syncwarp();
     PROF_MARK(13);
     const int NCHUNK = (int)(msgbytes / 16);
@@ -397,7 +379,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
     }
     PROF_MARK(14);
   };
-  cta_topk<R, K>(P, lev, trec, tk, lane, warp);
+  cta_topk<R, K>(P, lev, trec, tk, lane, warp, NW);
   if (warp == 0) publish(0);
 
   long long rounds = 0;
@@ -456,42 +438,82 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
     const int mode = st->mode;
     int lo = 0, hi = 0, gvend = 0;  // row-item range of this CTA, number of (g, v) pairs searched
     if (mode == 0) {
-      // ---- A2: rank the C*K list entries: thread (e, c2) counts the entries of
-      //      list c2 ahead of e (score desc, index asc, then list order); 16 lanes sum
+      // ---- A2: the NEc best merged list entries (warp 0): lane c holds the head of
+      //      CTA c's sorted list; NEc pops of the warp-wide best (score desc, index asc,
+      //      then list order; exhausted lists lose every tie)
       if (tid < NE) {
         wmeet[tid] = 0;
         wcover[tid] = 0;
       }
-      const int CK = C * K;
-      for (int b0 = 0; b0 < CK * 16; b0 += blockDim.x) {
-        const int t = b0 + tid;
-        const int e = t >> 4, c2 = t & 15;
-        int rk = 0;
-        if (e < CK) {
-          const int c = e / K, i = e - c * K;
-          if (c2 == c) {
-            rk = i;
-          } else if (c2 < C) {
-            const uint64_t ks = skey64(mb[c].list[i].s);
-            const uint32_t p = mb[c].list[i].p;
-            const int cl = c2 < c;
-#pragma unroll
-            for (int i2 = 0; i2 < K; ++i2) {
-              const uint64_t ko = skey64(mb[c2].list[i2].s);
-              const uint32_t po = mb[c2].list[i2].p;
-              rk += (int)((ko > ks) | ((ko == ks) & ((po < p) | ((po == p) & cl))));
+      if (warp == 0) {
+        int ptr = 0;
+        uint64_t key = 0;
+        uint32_t pp = NO_INDEX, valid = 0;
+        if (lane < C) {
+          key = skey64(mb[lane].list[0].s);
+          pp = mb[lane].list[0].p;
+          valid = 1;
+        }
+        for (int t = 0; t < NEc; ++t) {
+          const uint32_t hi = (uint32_t)(key >> 32), lo = (uint32_t)key;
+          const uint32_t mhi = __reduce_max_sync(0xffffffffu, hi);
+          unsigned m = __ballot_sync(0xffffffffu, hi == mhi);
+          if (m & (m - 1)) {
+            const uint32_t mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+            m = __ballot_sync(0xffffffffu, hi == mhi && lo == mlo);
+            if (m & (m - 1)) {
+              const bool in = (m >> lane) & 1u;
+              const uint32_t mp = __reduce_min_sync(0xffffffffu, in ? pp : NO_INDEX);
+              m = __ballot_sync(0xffffffffu, in && pp == mp);
+              if (m & (m - 1)) {
+                const bool in2 = (m >> lane) & 1u;
+                const uint32_t mv = __reduce_max_sync(0xffffffffu, in2 ? valid : 0u);
+                m = __ballot_sync(0xffffffffu, in2 && valid == mv);
+              }
+            }
+          }
+          if (lane == __ffs(m) - 1) {
+            sorted[t] = lane * K + ptr;
+            ++ptr;
+            if (ptr < K) {
+              key = skey64(mb[lane].list[ptr].s);
+              pp = mb[lane].list[ptr].p;
+            } else {
+              key = 0;
+              pp = NO_INDEX;
+              valid = 0;
             }
           }
         }
-#pragma unroll
-        for (int o = 8; o >= 1; o >>= 1) rk += __shfl_xor_sync(0xffffffffu, rk, o);
-        if (e < CK && c2 == 0 && rk < NEc) sorted[rk] = e;
       }
       PROF_MARK(3);
       __syncthreads();
+      // ---- A2b: update geometry of every window entry in every target dictionary,
+      //      seen from this CTA (Alg. 3 index sets), and its packed tile rect
+      for (int t = tid; t < NEc * W; t += blockDim.x) {
+        const int e = t / W, v = t - e * W;
+        const int src = sorted[e];
+        const RecT& r = mb[src / K].list[src % K];
+        VGeo gg;
+        gg.nr = 0;
+        gg.nc = 0;
+        gg.cntA = 0;
+        gg.cntB = 0;
+        gg.Tr = 0;
+        gg.t0 = 0;
+        gg.n0 = 0;
+        if (r.p != NO_INDEX) {
+          int u, k, j;
+          decode_p(r.p, sd, W, u, k, j);
+          vgeo<LGTW>(sp[u * W + v], sd[u], sd[v], k, j, rank, C, lgC, gg);
+        }
+        egeo[t] = gg;
+        rect[t] = pack_rect(gg);
+      }
+      __syncthreads();
       PROF_MARK(4);
-      // ---- A3: pairwise relations of the window entries (rects from the
-      //      publishers), one (a, v) pair per warp iteration, lane b:
+      // ---- A3: pairwise relations of the window entries, one (a, v) pair per
+      //      warp iteration, lane b:
       //      meet[a] bit b  -- tiles(a) and tiles(b) share a tile of dictionary v
       //      cover[a] bit b -- the tile of entry b lies in tiles(a)
       {
@@ -508,11 +530,10 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
         const int bN = bu >= 0 ? sd[bu].N : 1;
         for (int q = warp; q < NEc * W; q += NW) {
           const int a = q / W, v = q - a * W;
-          const int asrc = sorted[a];
-          const uint2 ra = mb[asrc / K].rect[(asrc % K) * W + v];
+          const uint2 ra = rect[a * W + v];
           bool meet = false, cover = false;
           if (lane < NEc && ra.x != 0u) {
-            meet = rects_meet(ra, mb[bsrc / K].rect[(bsrc % K) * W + v], sd[v].N);
+            meet = rects_meet(ra, rect[lane * W + v], sd[v].N);
             cover = bu == v && rect_has(ra, bj, bt, bN);
           }
           const unsigned mm = __ballot_sync(0xffffffffu, meet), cm = __ballot_sync(0xffffffffu, cover);
@@ -525,7 +546,8 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
       PROF_MARK(5);
       __syncthreads();
       PROF_MARK(6);
-      // ---- A4: the walk (warp 0, all lanes redundantly, bitmask logic) -----
+      // ---- A4: the walk (warp 0, all lanes redundantly, bitmask logic); warps 1..
+      //      meanwhile compute every window entry's update geometry seen from this CTA
       if (warp == 0) {
         const bool have = lane < NEc;
         const int src = have ? sorted[lane] : 0;
@@ -613,17 +635,9 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
             en.Et = 2.0 * (X2 + Y2 + rre * (X2 - Y2) - 2.0 * rim * XY);
           }
           ent[g] = en;
+          st->pick[g] = lane;
         }
         __syncwarp();
-        // update geometry of candidate g in dictionary v, seen from this CTA: lane
-        // handles the pairs (g, v) = lane + 32 s
-        for (int t = lane; t < G * W; t += 32) {
-          const int g = t / W, v = t - g * W;
-          const Ent& en = ent[g];
-          VGeo gg;
-          vgeo<LGTW>(sp[en.u * W + v], sd[en.u], sd[v], en.k, en.j, rank, C, lgC, gg);
-          egeo[t] = gg;
-        }
         // E recurrence and the energy stop rules (Z15) in selection order
         int Gs = 0, stopr = 0;
         if (lane == 0) {
@@ -669,7 +683,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
           int nrw = 0, ntl = 0;
           const int g = t >> 4, v = t & 15;
           if (t < GW && v < W && !P.floor_mode) {
-            const VGeo& gg = egeo[g * W + v];
+            const VGeo& gg = egeo[st->pick[g] * W + v];
             const int rows = gg.nc > 0 ? gg.cntA + gg.cntB : 0;
             nrw = rows * ((gg.Tr + 1) >> 1);
             ntl = rows * gg.Tr;
@@ -723,7 +737,8 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
     }
     ++rounds;
     // ---- B. residual update (or roll-back) over this CTA's rows ------------
-    // tile bookkeeping: record, candidate maximum, dirty level-0 node (no returns)
+    // tile bookkeeping: record, candidate maximum, dirty level-0 node (stamp + list)
+    const int stampv = round + 1;
     auto finish = [&](int l, int g, R bs, uint32_t bp, R bre, R bim) {
       if (lane == warp_argmax_lane(bs, bp)) {
         RecT rec;
@@ -735,7 +750,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
         trec[l] = rec;
         if (mode == 0) atomicMax(&vkey[g], score_key(bs));
         const int node = l >> 5;
-        atomicOr(&dirty[node >> 5], 1u << (node & 31));
+        if (atomicExch(&stamp[node], stampv) != stampv) list[atomicAdd(&cnt[0], 1)] = node;
       }
     };
     for (int gi = lo + warp; gi < hi; gi += NW) {
@@ -753,7 +768,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
         gv = (int)__reduce_add_sync(0xffffffffu, (unsigned)c);
       }
       const int g = gv >> 4, v = gv & 15;
-      const VGeo& gg = egeo[g * W + v];
+      const VGeo& gg = egeo[st->pick[g] * W + v];
       const DictGeo& dv = sd[v];
       const int Tr = gg.Tr, t0 = gg.t0, MR = dv.MR;
       const int hp = (Tr + 1) >> 1;
@@ -859,65 +874,34 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
     }
     PROF_MARK(11);
     __syncthreads();
-    // ---- C. level-0 refresh of the dirty nodes (set bits of the level-0 words)
-    {
-      const int nw = dw_off[1];
-      // every warp enumerates the same set bits; the r-th goes to warp r mod NW
-      int base = 0;
-      for (int w0 = 0; w0 < nw; w0 += 32) {
-        const uint32_t word = w0 + lane < nw ? dirty[w0 + lane] : 0u;
-        const int cntw = __popc(word);
-        int incl = cntw;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += y;
-        }
-        const int total = __shfl_sync(0xffffffffu, incl, 31);
-        const int first = (warp - base % NW + NW) % NW;  // first rank of this warp in this chunk
-        for (int rr = first; rr < total; rr += NW) {
-          const unsigned hold = __ballot_sync(0xffffffffu, incl > rr && incl - cntw <= rr);
-          const int src = __ffs(hold) - 1;
-          uint32_t wd = __shfl_sync(0xffffffffu, word, src);
-          const int k = rr - __shfl_sync(0xffffffffu, incl - cntw, src);
-          for (int q = 0; q < k; ++q) wd &= wd - 1u;  // drop the k lower set bits
-          const int node = (w0 + src) * 32 + __ffs(wd) - 1;
-          const long long c = (long long)node * 32 + lane;
-          const RecT rc = c < P.Lc ? trec[c] : empty_rec(R(0));
-          if (lane == warp_argmax_lane(rc.s, rc.p)) {
-            lev[node] = rc;
-            if (P.nlev > 1) atomicOr(&dirty[dw_off[1] + (node >> 10)], 1u << ((node >> 5) & 31));
+    // ---- C. level-0 refresh of the dirty nodes, then the upper levels, one level
+    //      at a time, nodes spread over the warps
+    for (int l = 0; l < P.nlev; ++l) {
+      const int nl = cnt[l];
+      const RecT* child = l == 0 ? trec : lev + P.lev_off[l - 1];
+      const long long nchild = l == 0 ? P.Lc : (long long)P.lev_n[l - 1];
+      for (int idx = warp; idx < nl; idx += NW) {
+        const int node = list[(l == 0 ? 0 : P.lev_off[l]) + idx];
+        const long long c = (long long)node * 32 + lane;
+        const RecT rc = c < nchild ? child[c] : empty_rec(R(0));
+        if (lane == warp_argmax_lane(rc.s, rc.p)) {
+          lev[(l == 0 ? 0 : P.lev_off[l]) + node] = rc;
+          if (l + 1 < P.nlev) {
+            const int par2 = node >> 5;
+            int* st2 = stamp + P.lev_off[l + 1];
+            if (atomicExch(&st2[par2], stampv) != stampv) list[P.lev_off[l + 1] + atomicAdd(&cnt[l + 1], 1)] = par2;
           }
         }
-        base += total;
       }
+      __syncthreads();
     }
-    __syncthreads();
     PROF_MARK(12);
-    // ---- D. upper levels, top-K, publish (warp 0) ---------------------------
-    if (warp == 0) {
-      for (int l = 1; l < P.nlev; ++l) {
-        for (int w0 = dw_off[l]; w0 < dw_off[l + 1]; ++w0) {
-          uint32_t word = dirty[w0];
-          while (word) {
-            const int b = __ffs(word) - 1;
-            word &= word - 1u;
-            const int node = (w0 - dw_off[l]) * 32 + b;
-            const int c = node * 32 + lane;
-            const RecT rc = c < P.lev_n[l - 1] ? lev[P.lev_off[l - 1] + c] : empty_rec(R(0));
-            if (lane == warp_argmax_lane(rc.s, rc.p)) {
-              lev[P.lev_off[l] + node] = rc;
-              if (l + 1 < P.nlev) atomicOr(&dirty[dw_off[l + 1] + (node >> 10)], 1u << ((node >> 5) & 31));
-            }
-            __syncwarp();
-          }
-        }
-      }
-      for (int i = lane; i < dw_off[P.nlev]; i += 32) dirty[i] = 0;
-      if (lane == 0 && mode == 1) st->G = 0;  // nothing to verify after a roll-back
+    if (tid == 0) {
+      for (int l = 0; l < P.nlev; ++l) cnt[l] = 0;
+      if (mode == 1) st->G = 0;  // nothing to verify after a roll-back
     }
     __syncthreads();
-    cta_topk<R, K>(P, lev, trec, tk, lane, warp);
+    cta_topk<R, K>(P, lev, trec, tk, lane, warp, NW);
     if (warp == 0) publish(par ^ 1);
   }
   if (rank == 0 && tid == 0) {

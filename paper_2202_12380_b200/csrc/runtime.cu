@@ -486,9 +486,9 @@ static int plan_grids(mpgabor* h, int64_t L, int TW) {
 // Automatic choice between the loop kernels (mpgabor_set_batch 0).  A multi-selection
 // round has a fixed cost of ~20k SM cycles (list exchange, ranking, walk, top-K) and
 // yields ~5 atoms; an iteration of the one-selection loop costs ~5k cycles plus its
-// share of the update.  Measured on B200 (DESIGN.md §8): multi-selection wins while
-// an atom's update is small (C1: 675 coefficients, 2.1 vs 2.6 us/atom), breaks even
-// near C2 (2,176) and loses on C3/C4 (18.5k / 56k).  Estimate the mean update size
+// share of the update.  Measured on B200 (DESIGN.md §6b): multi-selection wins while
+// an atom's update is small (C1: 675 coefficients, 1.89 vs 2.51 us/atom; C2: 2,176,
+// 2.57 vs 2.72) and loses on C3/C4 (18.5k / 56k).  Estimate the mean update size
 // from the kernel boxes (subsampled per target, averaged over the selected dictionary)
 // and require it to be a small fraction of the grid.
 static double mean_update(const mpgabor* h) {
@@ -506,7 +506,7 @@ static bool auto_multi(const mpgabor* h) {
   const double per_atom = mean_update(h);
   // rounds need independent atoms: small patches relative to the grid (C0's patch
   // covers 2.6 % of its grid and gives ~2 atoms per round)
-  return per_atom < 1500.0 && per_atom < 0.005 * (double)h->P_R;
+  return per_atom < 3000.0 && per_atom < 0.005 * (double)h->P_R;
 }
 
 // loop parameters for (TW, srec, C); returns shared-memory bytes (SIZE_MAX if the tree is too deep)
