@@ -233,6 +233,25 @@ def run_reference(args, cfg, rank, world):
 
 
 # ---------------------------------------------------------------------------
+# multi-rank aggregation (replicas)
+# ---------------------------------------------------------------------------
+def aggregate(times_ms, counts, world, device=None):
+    """Whole-job numbers over `world` replicas: every timed region is the MAX over ranks
+    (the slowest replica bounds the job), every count the SUM.  Returns (times, counts) as
+    Python floats; world == 1 returns them unchanged.  Works with any process group
+    backend (nccl on the GPU box, gloo in the CPU tests)."""
+    if world <= 1:
+        return [float(t) for t in times_ms], [float(c) for c in counts]
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(v) for v in times_ms], dtype=torch.float64, device=device)
+    c = torch.tensor([float(v) for v in counts], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(c, op=dist.ReduceOp.SUM)
+    return t.tolist(), c.tolist()
+
+
+# ---------------------------------------------------------------------------
 # native arm
 # ---------------------------------------------------------------------------
 def run_native(args, cfg, rank, world, local_rank):
@@ -296,14 +315,7 @@ def run_native(args, cfg, rank, world, local_rank):
     launches = mp.launch_count() - launches0
     step_ms = [a.elapsed_time(b) for a, b in ev]
     t_ms = float(sum(step_ms))
-    if world > 1:
-        tt = torch.tensor([t_ms, float(iters)], dtype=torch.float64, device=dev)
-        tmax = tt.clone()
-        dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
-        dist.all_reduce(tt[1:], op=dist.ReduceOp.SUM)
-        t_ms_max, total_iters = float(tmax[0]), float(tt[1])
-    else:
-        t_ms_max, total_iters = t_ms, float(iters)
+    (t_ms_max,), (total_iters,) = aggregate([t_ms], [iters], world, dev)
 
     # roofline of the dominant kernel (the persistent loop): algorithmic bytes / loop time
     out = mp.run(xd, maxit, cfg.errdb, bufs=bufs)
@@ -338,7 +350,8 @@ def run_native(args, cfg, rank, world, local_rank):
         e2e_iters += r.n_atoms
         d2h = r.n_atoms * 32 + (r.n_atoms + 1) * 8 + cfg.Ls * 8
     mpg.mpgabor_destroy(hh)
-    e2e_value = e2e_iters / (e2e_ms * 1e-3) * (world if world > 1 else 1)
+    (e2e_ms,), (e2e_iters,) = aggregate([e2e_ms], [e2e_iters], world, dev)
+    e2e_value = e2e_iters / (e2e_ms * 1e-3)
 
     clocks = clk.summary()
     line = {
