@@ -416,7 +416,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
         if (acc > 0) {
           if (rank == 0 && P.sol)  // c(p) += c~ for the accepted atoms, in order (Alg. 1 step 2a)
             for (int g = 0; g < acc; ++g) {
-              const Ent& e = ent[g];
+              const Ent& e = ent[st->pick[g]];
               const DictGeo du = sd[e.u];
               double2* s = P.sol + du.off + (long long)e.j * du.MR + e.k;
               double2 c = *s;
@@ -432,83 +432,123 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
       }
       PROF_MARK(1);
     }
+    if (warp != 0 || NW == 1) {
+      const bool prof1 = P.prof != nullptr && rank == 0 && tid == 32;
+      const long long tw0 = prof1 ? clock64() : 0;
+      if (warp != 0) mbar_wait(smem_addr(&mbar[par]), (uint32_t)((round >> 1) & 1));
+      const long long tw1 = prof1 ? clock64() : 0;
+      // ---- A2: window ranking, in parallel with the verification: merged position
+      //      of every published list entry = the number of entries ahead of it in
+      //      the total order (score key desc, index asc; empty records: list order),
+      //      4 lanes per entry; the NEc first positions name the walk window
+      const int NL = C * K;
+      const int rw = NW == 1 ? 0 : warp - 1, nrw = NW == 1 ? 1 : NW - 1;
+      for (int grp = rw; grp * 8 < NL; grp += nrw) {
+        const int e = grp * 8 + (lane >> 2), sub = lane & 3;
+        int c = 0;
+        if (e < NL) {
+          const RecT& re = mb[e / K].list[e % K];
+          const uint64_t ke = skey64(re.s);
+          const uint32_t pe = re.p;
+#pragma unroll
+          for (int i = 0; i < MAX_CLUSTER * K / 4; ++i) {  // every load issued before the compares
+            const int f = sub + 4 * i;   // f < MAX_CLUSTER * K: inside the mail array
+            const RecT& rf = mb[f / K].list[f % K];
+            const uint64_t kf = skey64(rf.s);
+            const uint32_t pf = rf.p;
+            // branch-free: (kf, -pf, -f) > (ke, -pe, -e), counted for f < NL only
+            const bool ahead = (kf > ke) | ((kf == ke) & ((pf < pe) | ((pf == pe) & (f < e))));
+            c += (int)(ahead & (f < NL));
+          }
+        }
+        c += __shfl_xor_sync(0xffffffffu, c, 1);
+        c += __shfl_xor_sync(0xffffffffu, c, 2);
+        if (e < NL && sub == 0 && c < NEc) sorted[c] = e;
+      }
+      if (prof1) {
+        const long long tw2 = clock64();
+        atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 30, (unsigned long long)(tw1 - tw0));
+        atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 31, (unsigned long long)(tw2 - tw1));
+      }
+    }
     __syncthreads();
-    if (warp != 0) mbar_wait(smem_addr(&mbar[par]), (uint32_t)((round >> 1) & 1));  // completed: acquire only
     PROF_MARK(2);
     const int mode = st->mode;
     int lo = 0, hi = 0, gvend = 0;  // row-item range of this CTA, number of (g, v) pairs searched
     if (mode == 0) {
-      // ---- A2: the NEc best merged list entries (warp 0): lane c holds the head of
-      //      CTA c's sorted list; NEc pops of the warp-wide best (score desc, index asc,
-      //      then list order; exhausted lists lose every tie)
-      if (tid < NE) {
-        wmeet[tid] = 0;
-        wcover[tid] = 0;
-      }
-      if (warp == 0) {
-        int ptr = 0;
-        uint64_t key = 0;
-        uint32_t pp = NO_INDEX, valid = 0;
-        if (lane < C) {
-          key = skey64(mb[lane].list[0].s);
-          pp = mb[lane].list[0].p;
-          valid = 1;
-        }
-        for (int t = 0; t < NEc; ++t) {
-          const uint32_t hi = (uint32_t)(key >> 32), lo = (uint32_t)key;
-          const uint32_t mhi = __reduce_max_sync(0xffffffffu, hi);
-          unsigned m = __ballot_sync(0xffffffffu, hi == mhi);
-          if (m & (m - 1)) {
-            const uint32_t mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
-            m = __ballot_sync(0xffffffffu, hi == mhi && lo == mlo);
-            if (m & (m - 1)) {
-              const bool in = (m >> lane) & 1u;
-              const uint32_t mp = __reduce_min_sync(0xffffffffu, in ? pp : NO_INDEX);
-              m = __ballot_sync(0xffffffffu, in && pp == mp);
-              if (m & (m - 1)) {
-                const bool in2 = (m >> lane) & 1u;
-                const uint32_t mv = __reduce_max_sync(0xffffffffu, in2 ? valid : 0u);
-                m = __ballot_sync(0xffffffffu, in2 && valid == mv);
-              }
-            }
-          }
-          if (lane == __ffs(m) - 1) {
-            sorted[t] = lane * K + ptr;
-            ++ptr;
-            if (ptr < K) {
-              key = skey64(mb[lane].list[ptr].s);
-              pp = mb[lane].list[ptr].p;
-            } else {
-              key = 0;
-              pp = NO_INDEX;
-              valid = 0;
-            }
-          }
-        }
-      }
       PROF_MARK(3);
       __syncthreads();
       // ---- A2b: update geometry of every window entry in every target dictionary,
-      //      seen from this CTA (Alg. 3 index sets), and its packed tile rect
-      for (int t = tid; t < NEc * W; t += blockDim.x) {
-        const int e = t / W, v = t - e * W;
-        const int src = sorted[e];
-        const RecT& r = mb[src / K].list[src % K];
-        VGeo gg;
-        gg.nr = 0;
-        gg.nc = 0;
-        gg.cntA = 0;
-        gg.cntB = 0;
-        gg.Tr = 0;
-        gg.t0 = 0;
-        gg.n0 = 0;
-        if (r.p != NO_INDEX) {
-          int u, k, j;
-          decode_p(r.p, sd, W, u, k, j);
-          vgeo<LGTW>(sp[u * W + v], sd[u], sd[v], k, j, rank, C, lgC, gg);
+      //      seen from this CTA (Alg. 3 index sets), and its packed tile rect; and,
+      //      one thread per window entry, its decoded index and scalar step
+      //      (c~, E~ of Eqs. (19)-(20): c(p) of an entry that is picked is unchanged
+      //      by the round's earlier picks, so they are the sequential ones)
+      for (int t = tid; t < NEc * W + NEc; t += blockDim.x) {
+        if (t < NEc * W) {
+          const int e = t / W, v = t - e * W;
+          const int src = sorted[e];
+          const RecT& r = mb[src / K].list[src % K];
+          VGeo gg;
+          gg.nr = 0;
+          gg.nc = 0;
+          gg.cntA = 0;
+          gg.cntB = 0;
+          gg.Tr = 0;
+          gg.t0 = 0;
+          gg.n0 = 0;
+          if (r.p != NO_INDEX) {
+            int u, k, j;
+            decode_p(r.p, sd, W, u, k, j);
+            vgeo<LGTW>(sp[u * W + v], sd[u], sd[v], k, j, rank, C, lgC, gg);
+          }
+          egeo[t] = gg;
+          rect[t] = pack_rect(gg);
+        } else {
+          const int e = t - NEc * W;
+          const int src = sorted[e];
+          const RecT rl = mb[src / K].list[src % K];
+          Ent en;
+          en.u = -1;
+          en.k = 0;
+          en.j = 0;
+          en.tre = 0.0;
+          en.tim = 0.0;
+          en.Et = 0.0;
+          en.selfc = 0;
+          en.key = score_key(rl.s);
+          if (rl.p != NO_INDEX) {
+            decode_p(rl.p, sd, W, en.u, en.k, en.j);
+            const int u = en.u, k = en.k;
+            const int Mu = sd[u].M;
+            const bool selfc = (k == 0) || (2 * k == Mu);
+            en.selfc = selfc ? 1 : 0;
+            const double cre = (double)rl.re, cim = (double)rl.im;
+            if (selfc) {  // Z13
+              en.tre = cre;
+              en.tim = 0.0;
+              en.Et = cre * cre;
+            } else {      // Eqs. (19)-(20) with rho = h_uu(-2k, 0) (Z11/Z12)
+              int mu = (-2 * k) & (Mu - 1);
+              if (2 * mu > Mu) mu -= Mu;
+              double rre = 0.0, rim = 0.0, inv = 1.0;
+              const int ri = mu - rho_lo[u];
+              if (ri >= 0 && ri < rho_n[u]) {
+                const RhoEnt rv = srho[rho_off[u] + ri];
+                rre = rv.re;
+                rim = rv.im;
+                inv = rv.inv;
+              }
+              const double nre = cre - (rre * cre - rim * cim);
+              const double nim = cim + (rre * cim + rim * cre);
+              const double tre = nre * inv, tim = nim * inv;
+              const double X2 = tre * tre, Y2 = tim * tim, XY = tre * tim;
+              en.tre = tre;
+              en.tim = tim;
+              en.Et = 2.0 * (X2 + Y2 + rre * (X2 - Y2) - 2.0 * rim * XY);
+            }
+          }
+          ent[e] = en;
         }
-        egeo[t] = gg;
-        rect[t] = pack_rect(gg);
       }
       __syncthreads();
       PROF_MARK(4);
@@ -517,29 +557,27 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
       //      meet[a] bit b  -- tiles(a) and tiles(b) share a tile of dictionary v
       //      cover[a] bit b -- the tile of entry b lies in tiles(a)
       {
-        int bu = -1, bj = 0, bt = 0, bsrc = 0;
+        int bu = -1, bj = 0, bt = 0;
         if (lane < NEc) {
-          bsrc = sorted[lane];
-          const RecT& rb = mb[bsrc / K].list[bsrc % K];
-          if (rb.p != NO_INDEX) {
-            int bk;
-            decode_p(rb.p, sd, W, bu, bk, bj);
-            bt = bk >> LGTW;
-          }
+          const Ent& eb = ent[lane];
+          bu = eb.u;
+          bj = eb.j;
+          bt = eb.k >> LGTW;
         }
         const int bN = bu >= 0 ? sd[bu].N : 1;
-        for (int q = warp; q < NEc * W; q += NW) {
-          const int a = q / W, v = q - a * W;
-          const uint2 ra = rect[a * W + v];
-          bool meet = false, cover = false;
-          if (lane < NEc && ra.x != 0u) {
-            meet = rects_meet(ra, rect[lane * W + v], sd[v].N);
-            cover = bu == v && rect_has(ra, bj, bt, bN);
+        const int lb = lane < NEc ? lane : 0;
+        for (int a = warp; a < NEc; a += NW) {  // warp: entry a, all target dictionaries
+          unsigned mm = 0u, cm = 0u;
+          for (int v = 0; v < W; ++v) {
+            const uint2 ra = rect[a * W + v], rb = rect[lb * W + v];
+            const bool meet = (lane < NEc) & rects_meet(ra, rb, sd[v].N);
+            const bool cover = (lane < NEc) & (bu == v) & rect_has(ra, bj, bt, bN);
+            mm |= __ballot_sync(0xffffffffu, meet);
+            cm |= __ballot_sync(0xffffffffu, cover);
           }
-          const unsigned mm = __ballot_sync(0xffffffffu, meet), cm = __ballot_sync(0xffffffffu, cover);
-          if (lane == 0 && (mm | cm)) {
-            if (mm) atomicOr(&wmeet[a], mm);
-            if (cm) atomicOr(&wcover[a], cm);
+          if (lane == 0) {
+            wmeet[a] = mm;
+            wcover[a] = cm;
           }
         }
       }
@@ -558,111 +596,87 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
         const long long it0 = st->it;
         const long long rem = P.maxit - it0;
         const int Bm = rem < (long long)B ? (int)max(rem, 0LL) : B;
+        const unsigned mtl = lane < NEc ? wmeet[lane] : 0u, cvl = lane < NEc ? wcover[lane] : 0u;
+        const double Etl = lane < NEc ? ent[lane].Et : 0.0;
+        const uint32_t keyl = lane < NEc ? ent[lane].key : 0u;
+        PROF_MARK(29);
         unsigned excl = 0, picked = 0, low = 0;
         int G = 0;
         int why = 0, lastpos = 0;  // walk statistics (profile mode)
-        while (true) {
-          if (G >= Bm) {
-            why = 1;
-            break;
-          }
+        // branch-free steps (the state is warp-uniform): every step either picks the
+        // next available entry or ends the walk with reason `why`
+        bool done = false;
+#pragma unroll
+        for (int step = 0; step <= BMAX; ++step) {
           const unsigned avail = win & ~excl & ~low;
-          if (!avail) {
-            why = 2;
-            break;
-          }
-          const int nx = __ffs(avail) - 1;
-          lastpos = nx;
-          const unsigned bit = 1u << nx;
-          if (lastm & excl & (bit - 1u) & ~low) {  // a CTA list ran out before nx
-            why = 3;
-            break;
-          }
-          if (!(posm & bit)) {  // zero score (stop rule 4 at G = 0)
-            why = 4;
-            break;
-          }
-          const unsigned mt = wmeet[nx], cv = wcover[nx];
-          if (mt & picked) {  // tiles(nx) meet X
-            why = 5;
-            break;
-          }
-          picked |= bit;
-          excl |= cv | bit;
-          ++G;
-          if (lastm & bit) {  // its CTA list is consumed
-            why = 6;
-            break;
-          }
-          low = (bit << 1) - 1u;
+          const int nx = __ffs(avail) - 1;              // -1: none
+          const unsigned bit = avail & (0u - avail);    // its bit (0: none)
+          const unsigned mt = __shfl_sync(0xffffffffu, mtl, nx & 31), cv = __shfl_sync(0xffffffffu, cvl, nx & 31);
+          const bool e1 = G >= Bm;                               // B picks
+          const bool e2 = avail == 0u;                           // window exhausted
+          const bool e3 = (lastm & excl & (bit - 1u) & ~low) != 0u;  // a CTA list ran out before nx
+          const bool e4 = (posm & bit) == 0u;                    // zero score (stop rule 4 at G = 0)
+          const bool e5 = (mt & picked) != 0u;                   // tiles(nx) meet X
+          const int w = e1 ? 1 : (e2 ? 2 : (e3 ? 3 : (e4 ? 4 : (e5 ? 5 : 0))));
+          const bool take = !done & (w == 0);
+          why = (!done & (w != 0)) ? w : why;
+          done = done | (w != 0);
+          picked |= take ? bit : 0u;
+          excl |= take ? (cv | bit) : 0u;
+          G += take ? 1 : 0;
+          lastpos = take ? nx : lastpos;
+          const bool e6 = take & ((lastm & bit) != 0u);          // its CTA list is consumed
+          why = e6 ? 6 : why;
+          done = done | e6;
+          low = take ? (bit << 1) - 1u : low;
         }
+        PROF_MARK(27);
         if (prof) {
           atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 20, (unsigned long long)lastpos);
           atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 20 + why, 1ull);
         }
-        // candidate g = the g-th picked window entry: decode, scalar step (lane g)
-        if ((picked >> lane) & 1u) {
-          const int g = __popc(picked & ((1u << lane) - 1u));
-          Ent en;
-          decode_p(rl.p, sd, W, en.u, en.k, en.j);
-          en.key = score_key(rl.s);
-          const int u = en.u, k = en.k;
-          const int Mu = sd[u].M;
-          const bool selfc = (k == 0) || (2 * k == Mu);
-          en.selfc = selfc ? 1 : 0;
-          const double cre = (double)rl.re, cim = (double)rl.im;
-          if (selfc) {  // Z13
-            en.tre = cre;
-            en.tim = 0.0;
-            en.Et = cre * cre;
-          } else {      // Eqs. (19)-(20) with rho = h_uu(-2k, 0) (Z11/Z12)
-            int mu = (-2 * k) & (Mu - 1);
-            if (2 * mu > Mu) mu -= Mu;
-            double rre = 0.0, rim = 0.0, inv = 1.0;
-            const int ri = mu - rho_lo[u];
-            if (ri >= 0 && ri < rho_n[u]) {
-              const RhoEnt rv = srho[rho_off[u] + ri];
-              rre = rv.re;
-              rim = rv.im;
-              inv = rv.inv;
-            }
-            const double nre = cre - (rre * cre - rim * cim);
-            const double nim = cim + (rre * cim + rim * cre);
-            const double tre = nre * inv, tim = nim * inv;
-            const double X2 = tre * tre, Y2 = tim * tim, XY = tre * tim;
-            en.tre = tre;
-            en.tim = tim;
-            en.Et = 2.0 * (X2 + Y2 + rre * (X2 - Y2) - 2.0 * rim * XY);
-          }
-          ent[g] = en;
-          st->pick[g] = lane;
-        }
+        // candidate g = the g-th picked window entry (lane g records its position);
+        // E recurrence and the energy stop rules (Z15) in selection order, every lane
+        // redundantly on the shuffled E~ of the picks
+        if ((picked >> lane) & 1u) st->pick[__popc(picked & ((1u << lane) - 1u))] = lane;
         __syncwarp();
-        // E recurrence and the energy stop rules (Z15) in selection order
-        int Gs = 0, stopr = 0;
+        const int pl = lane < G ? st->pick[lane] : 0;
+        const double Etg = __shfl_sync(0xffffffffu, Etl, pl);
+        const uint32_t kmine = __shfl_sync(0xffffffffu, keyl, pl);
+        double Ecur = st->E, Emine = 0.0;
+        int Gs = G;
+#pragma unroll
+        for (int g = 0; g < BMAX; ++g) {   // E_{k+1} = E_k - E~ in selection order
+          const double eg = __shfl_sync(0xffffffffu, Etg, g);
+          if (g < Gs) {
+            if (Ecur <= P.Etol || Ecur < 0.0) {
+              Gs = g;
+            } else {
+              Ecur = Ecur - eg;
+              if (lane == g) Emine = Ecur;
+            }
+          }
+        }
+        int stopr = 0;
+        if (Gs == 0) {
+          if (it0 >= P.maxit) stopr = 1;
+          else if (Ecur <= P.Etol) stopr = 2;
+          else if (Ecur < 0.0) stopr = 3;
+          else stopr = 4;
+        }
+        if (P.floor_mode && Gs > 1) Gs = 1;
+        G = Gs;
+        if (lane < G) {
+          st->Enext[lane] = Emine;
+          st->ckey[lane] = kmine;
+        }
         if (lane == 0) {
-          double Ecur = st->E;
-          for (; Gs < G; ++Gs) {
-            if (Ecur <= P.Etol || Ecur < 0.0) break;
-            const Ent& e = ent[Gs];
-            Ecur = Ecur - e.Et;
-            st->Enext[Gs] = Ecur;
-            st->ckey[Gs] = e.key;
-          }
-          if (Gs == 0) {
-            if (it0 >= P.maxit) stopr = 1;
-            else if (Ecur <= P.Etol) stopr = 2;
-            else if (Ecur < 0.0) stopr = 3;
-            else stopr = 4;
-          }
-          if (P.floor_mode && Gs > 1) Gs = 1;
-          st->G = Gs;
+          st->G = G;
           st->stop = stopr;
         }
-        G = __shfl_sync(0xffffffffu, Gs, 0);
         __syncwarp();
         if (rank == 0 && lane < G) {  // atoms / energies (final once verified)
-          const Ent& e = ent[lane];
+          const Ent& e = ent[pl];
           AtomOut a;
           a.w = e.u;
           a.m = e.k;
@@ -671,8 +685,9 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
           a.re = e.tre;
           a.im = e.tim;
           P.atoms[it0 + lane] = a;
-          P.energy[it0 + lane + 1] = st->Enext[lane];
+          P.energy[it0 + lane + 1] = Emine;
         }
+        PROF_MARK(28);
         // this CTA's items (tile pairs of its rows) and tiles of (g, v), at index
         // t = g * 16 + v (g-major; v >= W contribute nothing): lane handles 4 pairs
         const int GW = G * 16;
@@ -804,7 +819,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
           finish(l0 + t, g, bs, bp, bre, bim);
         }
       } else {
-        const Ent& en = ent[g];
+        const Ent& en = ent[st->pick[g]];
         const PairGeo& pg = sp[en.u * W + v];
         const bool selfc = en.selfc != 0;
         // modulation omega_R^{(k' nu) mod R} of this row (Eq. (15))

@@ -12,7 +12,7 @@ import torch
 import siggen
 from paper_2202_12380_b200.mpgabor import MPGabor
 
-PH = ["wait", "verify", "b", "rank", "b", "pair", "b", "-", "-", "walk", "b", "items", "lvl1", "topk", "push"]
+PH = ["wait", "verify", "b", "rank", "geom+b", "pair", "b", "-", "-", "scan", "b", "items", "lvl1", "topk", "push"]
 cfgs = sys.argv[1].split(",") if len(sys.argv) > 1 else ["C2"]
 K = int(sys.argv[2]) if len(sys.argv) > 2 else 100000
 batches = [int(b) for b in sys.argv[3].split(",")] if len(sys.argv) > 3 else [8]
@@ -34,6 +34,8 @@ for name in cfgs:
               + " ".join(f"{p}={x / n:.0f}" for p, x in zip(PH, c[:15])) + " cycles/round", flush=True)
         print(f"   walk: mean last window position {c[20] / n:.1f}; ends: B {c[21]} window {c[22]} "
               f"list-exhausted {c[23]} zero/stop {c[24]} overlap {c[25]} last-entry {c[26]}", flush=True)
+        print(f"   warp 1: wait {c[30] / n:.0f} rank {c[31] / n:.0f}", flush=True)
+        print(f"   walk split: setup {c[29] / n:.0f} bitmask {c[27] / n:.0f} E+atoms {c[28] / n:.0f} item-scan {c[9] / n:.0f}", flush=True)
         if c[19]:
             print(f"   thread-0 items: {c[19]} ({c[19] / n:.2f}/round) setup {c[16] / c[19]:.0f} loads {c[17] / c[19]:.0f} "
                   f"update+bookkeeping {c[18] / c[19]:.0f} cycles/item", flush=True)
