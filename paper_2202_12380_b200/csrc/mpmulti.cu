@@ -208,9 +208,10 @@ __device__ __forceinline__ void cta_topk(const LoopParams& P, const Rec<R>* lev,
       } else {
         id = -1;
       }
-      warp_pop_k<K>(key, p, id, part + q * K, lane);
+      warp_pop_k<K>(key, p, id, nq == 1 ? tk : part + q * K, lane);  // one chunk: no merge
     }
     __syncthreads();
+    if (nq == 1) continue;
     if (warp == 0) {
       int id = lane < nq * K ? part[lane] : -1;
       uint64_t key = 0;
@@ -501,6 +502,8 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
             decode_p(r.p, sd, W, u, k, j);
             vgeo<LGTW>(sp[u * W + v], sd[u], sd[v], k, j, rank, C, lgC, gg);
           }
+          const int hp = (gg.Tr + 1) >> 1;   // tile pairs per row; its reciprocal for the items
+          gg.pad = hp > 1 ? (int)(0xFFFFFFFFu / (uint32_t)hp + 1u) : 0;
           egeo[t] = gg;
           rect[t] = pack_rect(gg);
         } else {
@@ -788,7 +791,8 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
       const int Tr = gg.Tr, t0 = gg.t0, MR = dv.MR;
       const int hp = (Tr + 1) >> 1;
       const int it = gi - st->ibase[gv];
-      const int i = it / hp;              // row among this CTA's rows of (g, v)
+      // row among this CTA's rows of (g, v): it / hp by the reciprocal (exact: it * hp < 2^32)
+      const int i = hp > 1 ? (int)__umulhi((uint32_t)it, (uint32_t)gg.pad) : it;
       const int tt = 2 * (it - i * hp);   // first tile of the pair
       const int r = i < gg.cntA ? gg.rhoA + (i << lgC) : gg.rA + gg.rhoB + ((i - gg.cntA) << lgC);
       int nrow = gg.n0 + r;
