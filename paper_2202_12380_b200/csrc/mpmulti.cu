@@ -181,6 +181,54 @@ __device__ __forceinline__ void warp_pop_k(uint64_t key, uint32_t p, int id, int
   }
 }
 
+// One warp, NC candidates per lane (lane holds candidates c * 32 + lane): the K best
+// (key desc, index asc) by pops of the lanes' sorted heads -- no barrier, no merge.
+// Writes the ids (-1 = none) to out[0..K-1].
+template <int K, int NC>
+__device__ __forceinline__ void warp_topk_nc(uint64_t (&k)[NC], uint32_t (&p)[NC], int (&id)[NC], int* out,
+                                             int lane) {
+  auto ce = [&](int a, int b) {  // compare-exchange: position a gets the better one
+    const bool sw = (k[b] > k[a]) | ((k[b] == k[a]) & (p[b] < p[a]));
+    const uint64_t tk = sw ? k[b] : k[a], uk = sw ? k[a] : k[b];
+    const uint32_t tp = sw ? p[b] : p[a], up = sw ? p[a] : p[b];
+    const int ti = sw ? id[b] : id[a], ui = sw ? id[a] : id[b];
+    k[a] = tk; k[b] = uk; p[a] = tp; p[b] = up; id[a] = ti; id[b] = ui;
+  };
+  static_assert(NC == 2 || NC == 4, "sorting network for 2 or 4 candidates per lane");
+  if constexpr (NC == 2) {
+    ce(0, 1);
+  } else {
+    ce(0, 1); ce(2, 3); ce(0, 2); ce(1, 3); ce(1, 2);
+  }
+#pragma unroll
+  for (int t = 0; t < K; ++t) {
+    const uint64_t key = k[0];
+    const uint32_t pp = p[0];
+    const uint32_t hi = (uint32_t)(key >> 32), lo = (uint32_t)key;
+    const uint32_t mhi = __reduce_max_sync(0xffffffffu, hi);
+    unsigned m = __ballot_sync(0xffffffffu, hi == mhi);
+    if (m & (m - 1)) {
+      const uint32_t mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+      m = __ballot_sync(0xffffffffu, hi == mhi && lo == mlo);
+      if (m & (m - 1)) {
+        const bool in = (m >> lane) & 1u;
+        const uint32_t mp = __reduce_min_sync(0xffffffffu, in ? pp : NO_INDEX);
+        m = __ballot_sync(0xffffffffu, in && pp == mp);
+      }
+    }
+    const bool me = lane == __ffs(m) - 1;
+    if (me) out[t] = pp == NO_INDEX ? -1 : id[0];
+#pragma unroll
+    for (int c = 0; c + 1 < NC; ++c) {  // the winner shifts its sorted list
+      k[c] = me ? k[c + 1] : k[c];
+      p[c] = me ? p[c + 1] : p[c];
+      id[c] = me ? id[c + 1] : id[c];
+    }
+    k[NC - 1] = me ? 0ull : k[NC - 1];
+    p[NC - 1] = me ? NO_INDEX : p[NC - 1];
+  }
+}
+
 // Exact top-K tiles of this CTA down its node tree, by all warps: at every level
 // the candidates are the children of the previous level's K winners (all nodes at
 // the top level; the top-K nodes of a level contain the top-K of the level below),
@@ -198,6 +246,33 @@ __device__ __forceinline__ void cta_topk(const LoopParams& P, const Rec<R>* lev,
     const int count = l >= 0 ? P.lev_n[l] : (int)P.Lc;
     const Rec<R>* arr = l >= 0 ? lev + P.lev_off[l] : trec;
     const int nq = first ? (count + 31) >> 5 : K;
+#ifndef MPG_TOPK_CHUNKS
+    if (nq <= 4) {  // <= 128 candidates: warp 0 alone, 4 per lane (the other warps wait)
+      if (warp == 0) {
+        uint64_t kk[4];
+        uint32_t pk[4];
+        int ik[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          int id = c < nq ? (first ? c * 32 + lane : (tk[c] >= 0 ? tk[c] * 32 + lane : -1)) : -1;
+          kk[c] = 0;
+          pk[c] = NO_INDEX;
+          if (id >= 0 && id < count) {
+            kk[c] = skey64(arr[id].s);
+            pk[c] = arr[id].p;
+          } else {
+            id = -1;
+          }
+          ik[c] = id;
+        }
+        __syncwarp();
+        warp_topk_nc<K, 4>(kk, pk, ik, tk, lane);
+        __syncwarp();
+      }
+      if (l == -1) __syncthreads();
+      continue;
+    }
+#endif
     for (int q = warp; q < nq; q += NW) {  // chunk q (fewer warps than chunks: several each)
       int id = first ? q * 32 + lane : (tk[q] >= 0 ? tk[q] * 32 + lane : -1);
       uint64_t key = 0;
