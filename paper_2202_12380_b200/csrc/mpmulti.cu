@@ -459,12 +459,14 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
   if (warp == 0) publish(0);
 
   long long rounds = 0;
+  long long tbusy0 = 0;
   for (int round = 0;; ++round) {
     const int par = round & 1;
     const MsgT* mb = mail + par * MAX_CLUSTER;
     // ---- A0/A1 (warp 0): messages of the previous round; verify its candidates
     if (warp == 0) {
       mbar_wait(smem_addr(&mbar[par]), (uint32_t)((round >> 1) & 1));
+      if (P.prof != nullptr && tid == 0) tbusy0 = clock64();
       PROF_MARK(0);
       if (lane == 0) mbar_arm(smem_addr(&mbar[par]), C * msgbytes);  // slot reused at round + 2
       const int Gp = st->G;
@@ -670,44 +672,50 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
         const RecT rl = have ? mb[src / K].list[src % K] : empty_rec(R(0));
         const unsigned lastm = __ballot_sync(0xffffffffu, have && (src % K) == K - 1);
         const unsigned posm = __ballot_sync(0xffffffffu, have && rl.p != NO_INDEX && rl.s > R(0));
-        const unsigned win = NEc >= 32 ? 0xffffffffu : ((1u << NEc) - 1u);
         const long long it0 = st->it;
         const long long rem = P.maxit - it0;
         const int Bm = rem < (long long)B ? (int)max(rem, 0LL) : B;
-        const unsigned mtl = lane < NEc ? wmeet[lane] : 0u, cvl = lane < NEc ? wcover[lane] : 0u;
         const double Etl = lane < NEc ? ent[lane].Et : 0.0;
         const uint32_t keyl = lane < NEc ? ent[lane].key : 0u;
+        uint32_t mtr[NE], cvr[NE];  // every entry's masks in every lane (broadcast loads)
+#pragma unroll
+        for (int j = 0; j < NE; ++j) {
+          mtr[j] = wmeet[j];
+          cvr[j] = wcover[j];
+        }
         PROF_MARK(29);
-        unsigned excl = 0, picked = 0, low = 0;
+        unsigned excl = 0, picked = 0;
         int G = 0;
         int why = 0, lastpos = 0;  // walk statistics (profile mode)
-        // branch-free steps (the state is warp-uniform): every step either picks the
-        // next available entry or ends the walk with reason `why`
-        bool done = false;
+        // the walk in window order, statically unrolled and branch-free (the state is
+        // warp-uniform): entry j is skipped if a pick covers its tile; otherwise it
+        // is picked or it ends the walk.  Passing a skipped entry that was the last
+        // of its CTA's list ends the walk at the next entry that is not skipped.
+        bool done = false, passed_last = false;
 #pragma unroll
-        for (int step = 0; step <= BMAX; ++step) {
-          const unsigned avail = win & ~excl & ~low;
-          const int nx = __ffs(avail) - 1;              // -1: none
-          const unsigned bit = avail & (0u - avail);    // its bit (0: none)
-          const unsigned mt = __shfl_sync(0xffffffffu, mtl, nx & 31), cv = __shfl_sync(0xffffffffu, cvl, nx & 31);
-          const bool e1 = G >= Bm;                               // B picks
-          const bool e2 = avail == 0u;                           // window exhausted
-          const bool e3 = (lastm & excl & (bit - 1u) & ~low) != 0u;  // a CTA list ran out before nx
-          const bool e4 = (posm & bit) == 0u;                    // zero score (stop rule 4 at G = 0)
-          const bool e5 = (mt & picked) != 0u;                   // tiles(nx) meet X
-          const int w = e1 ? 1 : (e2 ? 2 : (e3 ? 3 : (e4 ? 4 : (e5 ? 5 : 0))));
-          const bool take = !done & (w == 0);
-          why = (!done & (w != 0)) ? w : why;
-          done = done | (w != 0);
+        for (int j = 0; j < NE; ++j) {
+          const unsigned bit = 1u << j;
+          const bool inwin = j < NEc;
+          const bool skip = (excl & bit) != 0u;
+          const bool cand = inwin & !skip & !done;
+          const bool e1 = G >= Bm;                       // B picks
+          const bool e3 = passed_last;                   // a CTA list ran out before j
+          const bool e4 = (posm & bit) == 0u;            // zero score (stop rule 4 at G = 0)
+          const bool e5 = (mtr[j] & picked) != 0u;       // tiles(j) meet X
+          const int w = e1 ? 1 : (e3 ? 3 : (e4 ? 4 : (e5 ? 5 : 0)));
+          const bool take = cand & (w == 0);
+          why = (cand & (w != 0)) ? w : why;
+          done = done | (cand & (w != 0));
           picked |= take ? bit : 0u;
-          excl |= take ? (cv | bit) : 0u;
+          excl |= take ? cvr[j] : 0u;
           G += take ? 1 : 0;
-          lastpos = take ? nx : lastpos;
-          const bool e6 = take & ((lastm & bit) != 0u);          // its CTA list is consumed
+          lastpos = take ? j : lastpos;
+          const bool e6 = take & ((lastm & bit) != 0u);  // its CTA list is consumed
           why = e6 ? 6 : why;
           done = done | e6;
-          low = take ? (bit << 1) - 1u : low;
+          passed_last = passed_last | (inwin & skip & !done & ((lastm & bit) != 0u));
         }
+        why = done ? why : 2;                            // window exhausted
         PROF_MARK(27);
         if (prof) {
           atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 20, (unsigned long long)lastpos);
@@ -996,6 +1004,8 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
     }
     __syncthreads();
     cta_topk<R, K>(P, lev, trec, tk, lane, warp, NW);
+    if (P.prof != nullptr && tid == 0 && rank < 16)  // per-CTA busy time (receive -> publish), slots 40..55
+      atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 40 + rank, (unsigned long long)(clock64() - tbusy0));
     if (warp == 0) publish(par ^ 1);
   }
   if (rank == 0 && tid == 0) {
