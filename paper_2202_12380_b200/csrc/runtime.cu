@@ -575,12 +575,22 @@ static int ensure_layout(mpgabor* h, int64_t Ls) {
   // candidate launch plans, first schedulable wins
   struct Cand { int TW, srec; };
   std::vector<Cand> cands;
-  const int tws[2] = {h->TW_req ? h->TW_req : 64, h->TW_req ? h->TW_req : 128};
-  if (h->srec_req != 2) {
-    cands.push_back({tws[0], 1});
-    if (tws[1] != tws[0]) cands.push_back({tws[1], 1});
+  // automatic tile width: 64 (then 128) for the one-selection loop; 32 first for the
+  // multi-selection loop (its rounds are bound by the per-tile work of several atoms:
+  // narrower tiles load and rescan 2x fewer bins, profiles/r01_configs.md)
+  {
+    const int rc = plan_grids(h, L, 64);  // P_R for the automatic kernel choice
+    if (rc) return rc;
   }
-  if (h->srec_req != 1) cands.push_back({tws[0], 0});
+  const bool multi_wanted = !(h->batch == 1 || (h->batch == 0 && !auto_multi(h)));
+  std::vector<int> tws;
+  if (h->TW_req) tws = {h->TW_req};
+  else if (multi_wanted) tws = {32, 64, 128};
+  else tws = {64, 128};
+  if (h->srec_req != 2)
+    for (int tw : tws) cands.push_back({tw, 1});
+  if (h->srec_req != 1)
+    for (int tw : tws) cands.push_back({tw, 0});
   std::string why = "no candidate";
   bool ok = false;
   // the multi-selection kernel packs tile rects as (row 20 bits, rows 12 bits) and
