@@ -98,7 +98,10 @@ int loop_max_cluster(bool f64, bool srec, int TW, int threads, size_t smem, bool
 
 // exact multi-selection loop kernel (mpmulti.cu, the default): MULTI_K = length of
 // every CTA's published top-K tile list
-constexpr int MULTI_K = 4;
+#ifndef MPG_MULTI_K
+#define MPG_MULTI_K 4
+#endif
+constexpr int MULTI_K = MPG_MULTI_K;
 size_t multi_smem_bytes(const LoopParams& P, bool f64);
 int multi_max_batch();
 cudaError_t launch_multi_loop(const LoopParams& P, bool f64, int threads, cudaStream_t st);
