@@ -154,9 +154,10 @@ int mpgabor_last_passes(const mpgabor* h, int32_t* passes);
  * else 4 CTAs, so that many signals run at once on the 148 SMs; mpgabor_set_launch
  * overrides it; clusters that do not fit queue).  x_dev: device fp64[B][Ls]; atoms_dev: mpg_atom[B][maxit]; energy_dev:
  * double[B][maxit+1]; res: host mpg_result[B].  Every signal's results equal those
- * of mpgabor_run on it with the one-selection kernel (bit for bit).  Uses the
- * one-selection cluster kernel regardless of mpgabor_set_batch.  Synchronises
- * cuda_stream. */
+ * of mpgabor_run on it (bit for bit; every loop kernel gives the same atoms).  The
+ * loop kernel follows mpgabor_set_batch (0: the automatic choice, 1: one selection
+ * per iteration, 2..8: exact multi-selection); grid mode is not used for batches.
+ * Synchronises cuda_stream. */
 int mpgabor_run_batch(mpgabor* h, const double* x_dev, int32_t B, int64_t Ls, int64_t maxit, double errdb,
                       mpg_atom* atoms_dev, double* energy_dev, mpg_result* res, void* cuda_stream);
 /* Synthesis of the approximation from an atom list (Eq. (18)):

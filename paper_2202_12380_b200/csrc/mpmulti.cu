@@ -49,8 +49,17 @@ namespace {
 
 using namespace mpcore;
 
-constexpr int NE = 8;     // walk window: best merged list entries considered per round
-constexpr int BMAX = 8;   // candidates per round (upper bound; LoopParams::spec lowers it)
+#ifndef MPG_NE
+#define MPG_NE 8
+#endif
+#ifndef MPG_BMAX
+#define MPG_BMAX 8
+#endif
+constexpr int NE = MPG_NE;      // walk window: best merged list entries considered per round
+constexpr int BMAX = MPG_BMAX;  // candidates per round (upper bound; LoopParams::spec lowers it)
+static_assert(BMAX == 8 || BMAX == 16, "candidate slots: 8 or 16");
+static_assert(NE <= 16, "walk window <= 16 entries");
+constexpr int IPL = BMAX * 16 / 32;  // (candidate, dictionary) item bases per lane
 
 template <typename R, int K>
 struct Msg {              // published by every CTA to every CTA at the end of a round
@@ -373,11 +382,18 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
   int* rho_lo = reinterpret_cast<int*>(smem + L.rho_meta);
   int* rho_n = rho_lo + W;
   int* rho_off = rho_n + W;
-  RecT* grec = reinterpret_cast<RecT*>(P.rec) + (long long)rank * P.Lc;
+  // batched independent signals: cluster `slot` works on signal `slot` (its own grids,
+  // records, backups, atoms, energies, result; the kernels are shared)
+  const int slot = (int)(blockIdx.x / (unsigned)C);
+  const double E0s = P.E0v ? P.E0v[slot] : P.E0;
+  const double Etols = P.Etolv ? P.Etolv[slot] : P.Etol;
+  AtomOut* atoms_out = P.atoms + (long long)slot * P.slot_atoms;
+  double* energy_out = P.energy + (long long)slot * (P.slot_atoms + 1);
+  RecT* grec = reinterpret_cast<RecT*>(P.rec) + (long long)slot * C * P.Lc + (long long)rank * P.Lc;
   RecT* trec = SREC ? reinterpret_cast<RecT*>(smem + L.trec) : grec;
-  C2* grid = reinterpret_cast<C2*>(P.grid);
+  C2* grid = reinterpret_cast<C2*>(P.grid) + (long long)slot * P.slot_grid;
   const C2* kern = reinterpret_cast<const C2*>(P.kern);
-  C2* backup = reinterpret_cast<C2*>(P.backup) + (long long)rank * P.bk_cap * TW;
+  C2* backup = reinterpret_cast<C2*>(P.backup) + ((long long)slot * C + rank) * P.bk_cap * TW;
 
   // ---- load tables -------------------------------------------------------
   for (int i = tid; i < W * W; i += blockDim.x) sp[i] = P.pairs[i];
@@ -417,7 +433,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     mbar_arm(smem_addr(&mbar[0]), C * msgbytes);
     mbar_arm(smem_addr(&mbar[1]), C * msgbytes);
-    st->E = P.E0;
+    st->E = E0s;
     st->it = 0;
     st->G = 0;
     st->mode = 0;
@@ -426,7 +442,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
   }
   cluster.sync();
 
-  const bool prof = P.prof != nullptr && rank == 0 && tid == 0;
+  const bool prof = P.prof != nullptr && slot == 0 && rank == 0 && tid == 0;
   long long tprev = clock64();
 #define PROF_MARK(i)                                                                                     \
   if (prof) {                                                                                             \
@@ -466,7 +482,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
     // ---- A0/A1 (warp 0): messages of the previous round; verify its candidates
     if (warp == 0) {
       mbar_wait(smem_addr(&mbar[par]), (uint32_t)((round >> 1) & 1));
-      if (P.prof != nullptr && tid == 0) tbusy0 = clock64();
+      if (P.prof != nullptr && slot == 0 && tid == 0) tbusy0 = clock64();
       PROF_MARK(0);
       if (lane == 0) mbar_arm(smem_addr(&mbar[par]), C * msgbytes);  // slot reused at round + 2
       const int Gp = st->G;
@@ -474,12 +490,15 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
       if (Gp >= 2) {
         // V_l = max over CTAs of the candidate-l key; candidate i is accepted iff
         // max_{l<i} V_l < key(c(p_i)) for it and every earlier candidate
-        uint4 va = make_uint4(0, 0, 0, 0), vb = make_uint4(0, 0, 0, 0);
-        if (lane < C) {
-          va = *reinterpret_cast<const uint4*>(&mb[lane].vkey[0]);
-          vb = *reinterpret_cast<const uint4*>(&mb[lane].vkey[4]);
+        uint32_t vk[BMAX];
+#pragma unroll
+        for (int q = 0; q < BMAX / 4; ++q) {
+          const uint4 va = lane < C ? *reinterpret_cast<const uint4*>(&mb[lane].vkey[4 * q]) : make_uint4(0, 0, 0, 0);
+          vk[4 * q] = va.x;
+          vk[4 * q + 1] = va.y;
+          vk[4 * q + 2] = va.z;
+          vk[4 * q + 3] = va.w;
         }
-        const uint32_t vk[BMAX] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w};
         uint32_t run = 0;
 #pragma unroll
         for (int l = 0; l < BMAX - 1; ++l) {
@@ -492,7 +511,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
       }
       if (lane == 0) {
         if (acc > 0) {
-          if (rank == 0 && P.sol)  // c(p) += c~ for the accepted atoms, in order (Alg. 1 step 2a)
+          if (rank == 0 && slot == 0 && P.sol)  // c(p) += c~ for the accepted atoms, in order (Alg. 1 step 2a)
             for (int g = 0; g < acc; ++g) {
               const Ent& e = ent[st->pick[g]];
               const DictGeo du = sd[e.u];
@@ -735,7 +754,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
         for (int g = 0; g < BMAX; ++g) {   // E_{k+1} = E_k - E~ in selection order
           const double eg = __shfl_sync(0xffffffffu, Etg, g);
           if (g < Gs) {
-            if (Ecur <= P.Etol || Ecur < 0.0) {
+            if (Ecur <= Etols || Ecur < 0.0) {
               Gs = g;
             } else {
               Ecur = Ecur - eg;
@@ -746,7 +765,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
         int stopr = 0;
         if (Gs == 0) {
           if (it0 >= P.maxit) stopr = 1;
-          else if (Ecur <= P.Etol) stopr = 2;
+          else if (Ecur <= Etols) stopr = 2;
           else if (Ecur < 0.0) stopr = 3;
           else stopr = 4;
         }
@@ -770,17 +789,17 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
           a.flags = e.selfc;
           a.re = e.tre;
           a.im = e.tim;
-          P.atoms[it0 + lane] = a;
-          P.energy[it0 + lane + 1] = Emine;
+          atoms_out[it0 + lane] = a;
+          energy_out[it0 + lane + 1] = Emine;
         }
         PROF_MARK(28);
         // this CTA's items (tile pairs of its rows) and tiles of (g, v), at index
-        // t = g * 16 + v (g-major; v >= W contribute nothing): lane handles 4 pairs
+        // t = g * 16 + v (g-major; v >= W contribute nothing): lane handles IPL pairs
         const int GW = G * 16;
-        int r4[4], t4[4], rs = 0, ts = 0;
+        int r4[IPL], t4[IPL], rs = 0, ts = 0;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int t = lane * 4 + q;
+        for (int q = 0; q < IPL; ++q) {
+          const int t = lane * IPL + q;
           int nrw = 0, ntl = 0;
           const int g = t >> 4, v = t & 15;
           if (t < GW && v < W && !P.floor_mode) {
@@ -805,8 +824,8 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
         }
         int rr = ri - rs, tt = ti - ts;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int t = lane * 4 + q;
+        for (int q = 0; q < IPL; ++q) {
+          const int t = lane * IPL + q;
           if (t <= GW) {
             st->ibase[t] = rr;
             st->tbase[t] = tt;
@@ -814,7 +833,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
           rr += r4[q];
           tt += t4[q];
         }
-        if (lane == 31 && GW == 128) {
+        if (lane == 31 && GW == BMAX * 16) {
           st->ibase[GW] = ri;
           st->tbase[GW] = ti;
         }
@@ -859,13 +878,16 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
       // (g, v) of item gi: count the item bases <= gi (ibase is non-decreasing)
       int gv;
       {
-        const int4 b4 = *reinterpret_cast<const int4*>(&st->ibase[lane * 4]);
-        const int i0 = lane * 4;
         int c = 0;
-        c += (i0 + 0 >= 1 && i0 + 0 <= gvend && b4.x <= gi) ? 1 : 0;
-        c += (i0 + 1 >= 1 && i0 + 1 <= gvend && b4.y <= gi) ? 1 : 0;
-        c += (i0 + 2 <= gvend && b4.z <= gi) ? 1 : 0;
-        c += (i0 + 3 <= gvend && b4.w <= gi) ? 1 : 0;
+#pragma unroll
+        for (int h4 = 0; h4 < IPL / 4; ++h4) {
+          const int i0 = lane * IPL + 4 * h4;
+          const int4 b4 = *reinterpret_cast<const int4*>(&st->ibase[i0]);
+          c += (i0 + 0 >= 1 && i0 + 0 <= gvend && b4.x <= gi) ? 1 : 0;
+          c += (i0 + 1 >= 1 && i0 + 1 <= gvend && b4.y <= gi) ? 1 : 0;
+          c += (i0 + 2 <= gvend && b4.z <= gi) ? 1 : 0;
+          c += (i0 + 3 <= gvend && b4.w <= gi) ? 1 : 0;
+        }
         gv = (int)__reduce_add_sync(0xffffffffu, (unsigned)c);
       }
       const int g = gv >> 4, v = gv & 15;
@@ -1004,15 +1026,15 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
     }
     __syncthreads();
     cta_topk<R, K>(P, lev, trec, tk, lane, warp, NW);
-    if (P.prof != nullptr && tid == 0 && rank < 16)  // per-CTA busy time (receive -> publish), slots 40..55
+    if (P.prof != nullptr && slot == 0 && tid == 0 && rank < 16)  // per-CTA busy time (receive -> publish), slots 40..55
       atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 40 + rank, (unsigned long long)(clock64() - tbusy0));
     if (warp == 0) publish(par ^ 1);
   }
   if (rank == 0 && tid == 0) {
-    P.result->n_done = st->it;
-    P.result->stop = st->stop;
-    P.result->E_final = st->E;
-    P.result->rounds = rounds;
+    P.result[slot].n_done = st->it;
+    P.result[slot].stop = st->stop;
+    P.result[slot].E_final = st->E;
+    P.result[slot].rounds = rounds;
   }
   if (prof) P.prof[15] = rounds;
 #undef PROF_MARK
@@ -1025,7 +1047,7 @@ cudaError_t launch_t(const LoopParams& P, int threads, cudaStream_t st) {
   CUDA_OK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem_bytes));
   if (P.C > 8) CUDA_OK(cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(P.C, 1, 1);
+  cfg.gridDim = dim3(P.C * std::max(1, P.nslot), 1, 1);   // one cluster per signal
   cfg.blockDim = dim3(threads, 1, 1);
   cfg.dynamicSmemBytes = P.smem_bytes;
   cfg.stream = st;

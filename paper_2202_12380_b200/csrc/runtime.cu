@@ -77,7 +77,7 @@ struct mpgabor {
   int kind = 2;           // loop kernel: 0 mploop.cu, 2 mpmulti.cu
   bool force_single = false;  // multi-selection impossible for this layout: use mploop.cu
   bool gx = false;            // one-selection kernel as a cooperative grid (> 16 CTAs, global exchange)
-  bool batch_mode = false;    // batched signals: the one-selection cluster kernel, one cluster per signal
+  bool batch_mode = false;    // batched signals: one cluster per signal
   int batch_C = 16;           // batched signals: automatic cluster size per signal
   int pedantic = 0;           // 1: pedantic selection (Eq. (20) energies)
   DevBuf etolv;               // batched signals: per-signal stop levels
@@ -502,15 +502,16 @@ static double mean_update(const mpgabor* h) {
   return sum / W;
 }
 
-static bool auto_multi(const mpgabor* h) {
+static bool auto_multi(const mpgabor* h, int64_t P_R) {
   const double per_atom = mean_update(h);
   // rounds need independent atoms: small patches relative to the grid (C0's patch
   // covers 2.6 % of its grid and gives ~2 atoms per round)
   // fp32 halves the bytes and the arithmetic of every tile update, which moves the
   // break-even to wider updates (C3 fp32: 3.62 vs 4.69 us/atom; C4: 12.6 vs 9.1)
   const double limit = h->f64() ? 3000.0 : 25000.0;
-  return per_atom < limit && per_atom < 0.005 * (double)h->P_R;
+  return per_atom < limit && per_atom < 0.005 * (double)P_R;
 }
+static bool auto_multi(const mpgabor* h) { return auto_multi(h, h->P_R); }
 
 // loop parameters for (TW, srec, C); returns shared-memory bytes (SIZE_MAX if the tree is too deep)
 static size_t plan_loop(mpgabor* h, int TW, int srec, int C) {
@@ -607,7 +608,6 @@ static int ensure_layout(mpgabor* h, int64_t Ls) {
   // CTAs beat one 16-CTA cluster despite the global-memory exchange
   const bool single = h->batch == 1 || (h->batch == 0 && !auto_multi(h));
   const bool try_grid = h->cluster_req == 0 && single && mean_update(h) > 30000.0 && !h->batch_mode;
-  if (h->batch_mode) h->force_single = true;
   const bool force_single0 = h->force_single;
   for (int pass = try_grid ? 0 : 1; pass < 2 && !ok; ++pass) {
   int creq = pass == 0 ? 64 : (h->batch_mode && h->cluster_req > MAX_CLUSTER ? 0 : h->cluster_req);
@@ -703,8 +703,8 @@ extern "C" int mpgabor_launch_info(const mpgabor* h, int32_t* cluster, int32_t* 
 // ---------------------------------------------------------------------------
 // DGT + loop; etol_abs (nullable) replaces the stop level 10^(errdb/10) E_0 (resets)
 // B >= 1 independent signals of Ls samples (x_dev[B][Ls], atoms_dev[B][maxit],
-// energy_dev[B][maxit+1], res[B]): B > 1 runs the one-selection cluster kernel with one
-// cluster per signal (batched mode, no solution vector).
+// energy_dev[B][maxit+1], res[B]): B > 1 runs the loop kernel of the automatic choice (or
+// mpgabor_set_batch) with one cluster per signal (batched mode, no solution vector).
 static int run_impl(mpgabor* h, const double* x_dev, int64_t Ls, int64_t maxit, double errdb, const double* etol_abs,
                     mpg_atom* atoms_dev, double* energy_dev, double* coef_dev, mpg_result* res, void* stream,
                     int B = 1) {
@@ -717,9 +717,20 @@ static int run_impl(mpgabor* h, const double* x_dev, int64_t Ls, int64_t maxit, 
   if (B < 1 || (B > 1 && coef_dev)) return h->fail(MPG_EINVAL, "batched runs need B >= 1 and no solution vector");
   int rc = enter_device(h);
   if (rc) return rc;
-  // batched signals: the one-selection cluster kernel; smaller clusters let more signals
-  // run at once (measured aggregate it/s on B200, profiles/r01_batch.md)
-  const int bc = B <= 4 ? 16 : (B <= 12 ? 8 : 4);
+  // batched signals: one cluster per signal; smaller clusters let more signals run at
+  // once (measured aggregate it/s on B200, profiles/r01_batch.md)
+  int bc = B <= 4 ? 16 : (B <= 12 ? 8 : 4);
+  if (bc == 4) {
+    // multi-selection kernel: 4-CTA clusters only while the tile records still fit in
+    // shared memory (C1: 7.5 M it/s for 36 signals; C2 falls to 1.7 M with global
+    // records against 2.9 M on 8-CTA clusters, profiles/r01_batch.md)
+    const int64_t L = (Ls + ell_of(h) - 1) / ell_of(h) * ell_of(h);
+    int64_t P_R = 0;
+    for (int w = 0; w < h->W; ++w) P_R += (L / h->dicts[w].a) * (h->dicts[w].M / 2 + 1);
+    const bool multi = h->batch >= 2 || (h->batch == 0 && auto_multi(h, P_R));
+    const size_t rec_bytes = (size_t)(P_R / 4 / 32 + 1) * (h->f64() ? sizeof(Rec<double>) : sizeof(Rec<float>));
+    if (multi && rec_bytes > 150 * 1024) bc = 8;
+  }
   if (h->batch_mode != (B > 1) || (B > 1 && bc != h->batch_C)) {
     h->batch_mode = B > 1;
     h->batch_C = bc;
@@ -733,6 +744,7 @@ static int run_impl(mpgabor* h, const double* x_dev, int64_t Ls, int64_t maxit, 
   if (B > 1) {
     TRY_CUDA(h, h->grid.ensure(h->celem() * h->grid_elems * B));
     TRY_CUDA(h, h->rec.ensure((h->f64() ? sizeof(Rec<double>) : sizeof(Rec<float>)) * P.C * P.Lc * B));
+    if (h->kind == 2) TRY_CUDA(h, h->backup.ensure(h->celem() * (size_t)h->TW * P.bk_cap * P.C * B));
   }
   TRY_CUDA(h, h->E0.ensure(sizeof(double) * B));
   TRY_CUDA(h, h->result.ensure(sizeof(LoopResult) * B));

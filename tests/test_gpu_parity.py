@@ -470,12 +470,17 @@ def test_reset_every_large_equals_run(mpg):
 # ---------------------------------------------------------------------------
 # batched independent signals: one cluster per signal
 # ---------------------------------------------------------------------------
-@pytest.mark.parametrize("name,prec,B,K", [("C1", "f64", 4, 2000), ("C2", "f64", 10, 1500), ("C1", "f32", 3, 1500)])
-def test_batch_equals_individual_runs(mpg, name, prec, B, K):
+@pytest.mark.parametrize("kernel", [0, 1])   # automatic (multi-selection for C1/C2), one selection
+@pytest.mark.parametrize("name,prec,B,K", [("C1", "f64", 4, 2000), ("C2", "f64", 10, 1500), ("C1", "f32", 3, 1500),
+                                           ("C1", "f64", 20, 1000)])
+def test_batch_equals_individual_runs(mpg, name, prec, B, K, kernel):
     cfg = CONFIGS[name]
     X = np.stack([siggen.signal(cfg, seed=cfg.seed + 100 * b) for b in range(B)])
     mp = mpg.MPGabor(cfg.dicts, cfg.thr, prec)
+    mp.set_batch(kernel)
     outs = mp.run_batch(torch.from_numpy(X).cuda(), K, cfg.errdb)
+    if kernel == 0 and name in ("C1", "C2"):   # the multi-selection kernel ran
+        assert all(o.rounds < o.n for o in outs)
     mp.set_batch(1)
     for b in range(B):
         one = mp.run(torch.from_numpy(X[b]).cuda(), K, cfg.errdb)

@@ -1,5 +1,5 @@
 """Dev tool: batched independent decompositions (mpgabor_run_batch) -- aggregate MP
-iterations/s over B signals of a config (one 16-CTA cluster each), vs one signal.
+iterations/s over B signals of a config (one cluster each, automatic size and loop kernel), vs one signal.
 Writes profiles/<tag>_batch.md."""
 import os
 import sys
@@ -18,7 +18,7 @@ for name in cfgs:
     cfg = siggen.CONFIGS[name]
     for prec in ("f64",):
         mp = MPGabor(cfg.dicts, cfg.thr, prec)
-        for B in (1, 4, 9, 18, 36):
+        for B in (1, 4, 9, 18, 36, 72):
             X = torch.from_numpy(np.stack([siggen.signal(cfg, seed=cfg.seed + 100 * b) for b in range(B)])).cuda()
             mp.run_batch(X, cfg.maxit, cfg.errdb)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -28,15 +28,17 @@ for name in cfgs:
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1)
             atoms = sum(o.n for o in outs)
-            rows.append((name, prec, B, atoms, ms, atoms / (ms * 1e-3), mp.last_timing()[2], mp.launch_info()["cluster"]))
+            kern = "multi" if outs[0].rounds < outs[0].n else "single"
+            rows.append((name, prec, B, atoms, ms, atoms / (ms * 1e-3), mp.last_timing()[2], mp.launch_info()["cluster"], kern))
             print(rows[-1], flush=True)
         mp.close()
 os.makedirs("profiles", exist_ok=True)
 with open(f"profiles/{tag}_batch.md", "w") as f:
     f.write("# Batched independent signals (mpgabor_run_batch), B200\n\n")
-    f.write("B signals of the config (seeds seed + 100 b), each decomposed to its stop rule by its own 16-CTA "
-            "cluster; time = CUDA events around the whole call (DGT of every signal, tile init, loop, result copy); "
+    f.write("B signals of the config (seeds seed + 100 b), each decomposed to its stop rule by its own "
+            "cluster (automatic cluster size and loop kernel: multi-selection for C1/C2); time = CUDA events "
+            "around the whole call (DGT of every signal, tile init, loop, result copy); "
             "aggregate = total selections / time.\n\n")
-    f.write("| config | prec | B | CTAs per signal | selections | ms | aggregate it/s | loop ms |\n|---|---|---|---|---|---|---|---|\n")
+    f.write("| config | prec | B | kernel | CTAs per signal | selections | ms | aggregate it/s | loop ms |\n|---|---|---|---|---|---|---|---|---|\n")
     for r in rows:
-        f.write(f"| {r[0]} | {r[1]} | {r[2]} | {r[7]} | {r[3]} | {r[4]:.2f} | {r[5]:.0f} | {r[6]:.2f} |\n")
+        f.write(f"| {r[0]} | {r[1]} | {r[2]} | {r[8]} | {r[7]} | {r[3]} | {r[4]:.2f} | {r[5]:.0f} | {r[6]:.2f} |\n")
