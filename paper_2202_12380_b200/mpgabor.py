@@ -372,8 +372,9 @@ class MPGabor:
         en = energy[: n + 1].cpu().numpy()
         return RunOutput(at, en, res.stop_reason, res.E0, res.L_pad, res.cluster, None, atoms, res.rounds)
 
-    def run_batch(self, X, maxit, errdb=-math.inf, stream=None):
-        """B independent signals X[B][Ls] (one cluster each); returns a list of RunOutput."""
+    def run_batch(self, X, maxit, errdb=-math.inf, stream=None, fetch=True):
+        """B independent signals X[B][Ls] (one cluster each); returns a list of RunOutput
+        (fetch=False: the list of mpg_result and the device atom / energy buffers)."""
         torch = self.torch
         if not isinstance(X, torch.Tensor):
             X = torch.as_tensor(np.ascontiguousarray(X, dtype=np.float64)).cuda()
@@ -382,6 +383,8 @@ class MPGabor:
         atoms = torch.empty(B * max(int(maxit), 1) * ATOM_DTYPE.itemsize, dtype=torch.uint8, device="cuda")
         energy = torch.empty(B * (int(maxit) + 1), dtype=torch.float64, device="cuda")
         res = mpgabor_run_batch(self.h, X, B, Ls, maxit, errdb, atoms, energy, stream)
+        if not fetch:
+            return res, atoms, energy
         ab = atoms.cpu().numpy().tobytes()
         en = energy.cpu().numpy()
         outs = []

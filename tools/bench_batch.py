@@ -20,15 +20,15 @@ for name in cfgs:
         mp = MPGabor(cfg.dicts, cfg.thr, prec)
         for B in (1, 4, 9, 18, 36, 72):
             X = torch.from_numpy(np.stack([siggen.signal(cfg, seed=cfg.seed + 100 * b) for b in range(B)])).cuda()
-            mp.run_batch(X, cfg.maxit, cfg.errdb)
+            mp.run_batch(X, cfg.maxit, cfg.errdb, fetch=False)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            outs = mp.run_batch(X, cfg.maxit, cfg.errdb)
+            res, _, _ = mp.run_batch(X, cfg.maxit, cfg.errdb, fetch=False)   # synchronises; no host copies
             e1.record()
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1)
-            atoms = sum(o.n for o in outs)
-            kern = "multi" if outs[0].rounds < outs[0].n else "single"
+            atoms = sum(r.n_atoms for r in res)
+            kern = "multi" if res[0].rounds < res[0].n_atoms else "single"
             rows.append((name, prec, B, atoms, ms, atoms / (ms * 1e-3), mp.last_timing()[2], mp.launch_info()["cluster"], kern))
             print(rows[-1], flush=True)
         mp.close()
@@ -37,7 +37,8 @@ with open(f"profiles/{tag}_batch.md", "w") as f:
     f.write("# Batched independent signals (mpgabor_run_batch), B200\n\n")
     f.write("B signals of the config (seeds seed + 100 b), each decomposed to its stop rule by its own "
             "cluster (automatic cluster size and loop kernel: multi-selection for C1/C2); time = CUDA events "
-            "around the whole call (DGT of every signal, tile init, loop, result copy); "
+            "around the whole C-ABI call (DGT of every signal, tile init, loop, result copy; atoms stay on the "
+            "device); "
             "aggregate = total selections / time.\n\n")
     f.write("| config | prec | B | kernel | CTAs per signal | selections | ms | aggregate it/s | loop ms |\n|---|---|---|---|---|---|---|---|---|\n")
     for r in rows:
