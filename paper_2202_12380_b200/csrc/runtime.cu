@@ -484,13 +484,14 @@ static int plan_grids(mpgabor* h, int64_t L, int TW) {
 }
 
 // Automatic choice between the loop kernels (mpgabor_set_batch 0).  A multi-selection
-// round has a fixed cost of ~20k SM cycles (list exchange, ranking, walk, top-K) and
+// round has a fixed cost of ~12k SM cycles (list exchange, ranking, walk, top-K) and
 // yields ~5 atoms; an iteration of the one-selection loop costs ~5k cycles plus its
 // share of the update.  Measured on B200: multi-selection wins while
-// an atom's update is small (C1: 675 coefficients, 1.89 vs 2.51 us/atom; C2: 2,176,
-// 2.57 vs 2.72) and loses on C3/C4 (18.5k / 56k).  Estimate the mean update size
-// from the kernel boxes (subsampled per target, averaged over the selected dictionary)
-// and require it to be a small fraction of the grid.
+// an atom's update is moderate (C1: 643 coefficients, 1.42 vs 2.52 us/atom; C2: 2,086,
+// 2.05 vs 2.72; C3: 18.6k) and loses on C4 (54k, where the one-selection loop runs on a
+// 64-CTA grid).  Estimate the mean update size from the kernel boxes (subsampled per
+// target, averaged over the selected dictionary) and require it to be a small fraction
+// of the grid.
 static double mean_update(const mpgabor* h) {
   const int W = h->W;
   double sum = 0.0;
@@ -506,9 +507,9 @@ static bool auto_multi(const mpgabor* h, int64_t P_R) {
   const double per_atom = mean_update(h);
   // rounds need independent atoms: small patches relative to the grid (C0's patch
   // covers 2.6 % of its grid and gives ~2 atoms per round)
-  // fp32 halves the bytes and the arithmetic of every tile update, which moves the
-  // break-even to wider updates (C3 fp32: 3.62 vs 4.69 us/atom; C4: 12.6 vs 9.1)
-  const double limit = h->f64() ? 3000.0 : 25000.0;
+  // break-even between C3 (18.6k coefficients per atom: 4.3 vs 5.0 us/atom fp64, 3.6 vs
+  // 4.7 fp32) and C4 (54k: 9.1 vs 7.5 fp64 on a 64-CTA grid)
+  const double limit = 30000.0;
   return per_atom < limit && per_atom < 0.005 * (double)P_R;
 }
 static bool auto_multi(const mpgabor* h) { return auto_multi(h, h->P_R); }
@@ -587,14 +588,14 @@ static int ensure_layout(mpgabor* h, int64_t Ls) {
     if (rc) return rc;
   }
   const bool multi_wanted = !(h->batch == 1 || (h->batch == 0 && !auto_multi(h)));
-  std::vector<int> tws;
-  if (h->TW_req) tws = {h->TW_req};
-  else if (multi_wanted) tws = {32, 64, 128};
-  else tws = {64, 128};
-  if (h->srec_req != 2)
-    for (int tw : tws) cands.push_back({tw, 1});
-  if (h->srec_req != 1)
-    for (int tw : tws) cands.push_back({tw, 0});
+  // multi-selection: narrow tiles matter more than shared-memory records (C3 fp64: 64-bin
+  // tiles with global records 4.31 us/atom, 128-bin tiles with shared records 6.66)
+  std::vector<Cand> pref;
+  if (h->TW_req) pref = {{h->TW_req, 1}, {h->TW_req, 0}};
+  else if (multi_wanted) pref = {{32, 1}, {64, 1}, {64, 0}, {32, 0}, {128, 1}, {128, 0}};
+  else pref = {{64, 1}, {128, 1}, {64, 0}, {128, 0}};
+  for (const Cand& c : pref)
+    if ((c.srec == 1 && h->srec_req != 2) || (c.srec == 0 && h->srec_req != 1)) cands.push_back(c);
   std::string why = "no candidate";
   bool ok = false;
   // the multi-selection kernel packs tile rects as (row 20 bits, rows 12 bits) and

@@ -104,12 +104,12 @@ with open(f"profiles/{tag}_configs.md", "w") as f:
     f.write("batch 0 = automatic kernel choice (the library default), 1 = one selection per iteration, "
             "8 = exact multi-selection.  Loop only (DGT separate); median of the runs.  Update/argmax split "
             "from CTA 0's per-phase clock64 sums.  Roofline = algorithmic update bytes / time / peak.\n\n")
-    f.write("| config | prec | batch | kernel | CTAs | atoms | rounds | it/s | us/it | touched/it | GB/s | frac | "
+    f.write("| config | prec | batch | kernel | CTAs | TW | atoms | rounds | it/s | us/it | touched/it | GB/s | frac | "
             "update us/it | update frac | argmax us/it | floor us/it | DGT ms |\n")
-    f.write("|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|\n")
+    f.write("|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|\n")
     for r in rows:
         fl = r.get("floor_us_per_it")
-        f.write(f"| {r['config']} | {r['precision']} | {r['batch']} | {r['kernel']} | {r['launch']['cluster']} | {r['atoms']} | {r['rounds']} | "
+        f.write(f"| {r['config']} | {r['precision']} | {r['batch']} | {r['kernel']} | {r['launch']['cluster']} | {r['launch']['tile_width']} | {r['atoms']} | {r['rounds']} | "
                 f"{r['it_per_s']:.0f} | {r['us_per_it']:.3f} | {r['touched_per_it']:.0f} | {r['achieved_gbs']:.1f} | "
                 f"{r['roofline_frac']:.4f} | {r['update_us_per_it']:.3f} | {r['update_roofline_frac']:.4f} | "
                 f"{r['argmax_us_per_it']:.3f} | {'' if fl is None else f'{fl:.3f}'} | {r['dgt_ms']:.2f} |\n")
