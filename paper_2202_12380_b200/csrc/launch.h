@@ -76,8 +76,10 @@ struct LoopParams {
   LoopResult* result;
   long long* prof;               // optional [8] clock64 phase sums (rank 0, thread 0), [7] = iterations
   int floor_mode;                // 1: skip the update (latency-floor measurement; results invalid)
-  void* gx_rec;                  // one-selection kernel, grid mode: Rec<R>[2][C] roots in global memory (else null)
-  unsigned long long* gx_stamp;  // [2][C] iteration stamps of gx_rec (zeroed before the launch)
+  int gx;                        // 1: grid mode (cooperative grid of C CTAs, exchange through global memory)
+  void* gx_rec;                  // grid mode: one-selection kernel Rec<R>[2][C] roots, multi-selection
+                                 //   kernel its [2][C] messages, in global memory (else null)
+  unsigned long long* gx_stamp;  // [2][C] round stamps of gx_rec (zeroed before the launch)
   const double* E0v;             // batched signals (one-selection cluster kernel): per-slot E_0, stop level
   const double* Etolv;           //   (null: the scalars E0 / Etol)
   long long slot_grid;           //   grid elements per slot; the records per slot are C * Lc
@@ -105,7 +107,9 @@ constexpr int MULTI_K = MPG_MULTI_K;
 size_t multi_smem_bytes(const LoopParams& P, bool f64);
 int multi_max_batch();
 cudaError_t launch_multi_loop(const LoopParams& P, bool f64, int threads, cudaStream_t st);
-int multi_max_cluster(bool f64, bool srec, int TW, int threads, size_t smem);
+// gx: the global-exchange grid kernel; returns its co-resident CTA count
+int multi_max_cluster(bool f64, bool srec, int TW, int threads, size_t smem, bool gx = false);
+size_t multi_msg_bytes(bool f64);
 
 
 // synthesis (synth.cu)

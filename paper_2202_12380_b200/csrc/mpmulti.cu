@@ -92,7 +92,7 @@ struct St {               // round state (shared memory)
 };
 
 struct Smem {
-  size_t mbar, mail, mymsg, trec, lev, ent, egeo, wmask, rect, st, vkey, sorted, tk, stamp, list, cnt, pairs, dicts, own, roots,
+  size_t mbar, mail, mymsg, trec, lev, ent, egeo, wmask, rect, st, vkey, sorted, hsel, tk, stamp, list, cnt, pairs, dicts, own, roots,
       rho, rho_meta, total;
 };
 
@@ -107,7 +107,7 @@ __host__ __device__ inline Smem smem_layout(const LoopParams& P, size_t recsz, s
   s.mbar = o;
   o += 32;
   s.mail = o;
-  o += 2 * MAX_CLUSTER * msgsz;
+  o += P.gx ? (size_t)P.C * msgsz : 2 * MAX_CLUSTER * msgsz;  // grid mode: one copy of the C messages
   s.mymsg = o;
   o += msgsz;
   s.trec = o;
@@ -133,6 +133,8 @@ __host__ __device__ inline Smem smem_layout(const LoopParams& P, size_t recsz, s
   s.vkey = o;
   o += sizeof(uint32_t) * BMAX;
   s.sorted = o;
+  o += sizeof(int) * NE;
+  s.hsel = o;                 // grid mode: the lists of the NE best heads
   o += sizeof(int) * NE;
   s.tk = o;
   o += sizeof(int) * 64;
@@ -341,14 +343,30 @@ __device__ __forceinline__ bool rect_has(uint2 a, int n, int t, int N) {
   return (d < ar) & (t >= at) & (t < at + aT);
 }
 
-template <typename R, int TW, bool SREC, int K>
+// grid-mode exchange (GX): a CTA's message and its round stamp in global memory; the
+// stamp is written with release and polled with acquire semantics (gpu scope)
+__device__ __forceinline__ void gx_st_release(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long gx_ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// GX = false: one thread-block cluster of C <= 16 CTAs exchanging messages through
+// distributed shared memory (st.async + mbarrier).  GX = true: a cooperative grid of C
+// CTAs (32..128, one per SM) exchanging them through global memory (release/acquire
+// stamps; the messages are copied into shared memory) and ranking the C*K entries in
+// two stages (the NE best list heads, then their lists' entries); everything else is
+// identical.
+template <typename R, int TW, bool SREC, int K, bool GX>
 __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
   using C2 = typename cplx<R>::t;
   using RecT = Rec<R>;
   using MsgT = Msg<R, K>;
-  cg::cluster_group cluster = cg::this_cluster();
   const int C = P.C, lgC = ilog2(P.C);
-  const int rank = (int)cluster.block_rank();
+  const int rank = GX ? (int)blockIdx.x : (int)cg::this_cluster().block_rank();
   const int W = P.W;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, NW = blockDim.x >> 5;
   constexpr int LGTW = TW == 32 ? 5 : (TW == 64 ? 6 : 7);
@@ -370,6 +388,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
   St* st = reinterpret_cast<St*>(smem + L.st);
   uint32_t* vkey = reinterpret_cast<uint32_t*>(smem + L.vkey);
   int* sorted = reinterpret_cast<int*>(smem + L.sorted);
+  int* hsel = reinterpret_cast<int*>(smem + L.hsel);
   int* tk = reinterpret_cast<int*>(smem + L.tk);
   int* stamp = reinterpret_cast<int*>(smem + L.stamp);   // dirty-node stamps and lists per level
   int* list = reinterpret_cast<int*>(smem + L.list);
@@ -384,7 +403,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
   int* rho_off = rho_n + W;
   // batched independent signals: cluster `slot` works on signal `slot` (its own grids,
   // records, backups, atoms, energies, result; the kernels are shared)
-  const int slot = (int)(blockIdx.x / (unsigned)C);
+  const int slot = GX ? 0 : (int)(blockIdx.x / (unsigned)C);
   const double E0s = P.E0v ? P.E0v[slot] : P.E0;
   const double Etols = P.Etolv ? P.Etolv[slot] : P.Etol;
   AtomOut* atoms_out = P.atoms + (long long)slot * P.slot_atoms;
@@ -428,11 +447,13 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
   }
   const uint32_t msgbytes = (uint32_t)sizeof(MsgT);
   if (tid == 0) {
-    mbar_init(smem_addr(&mbar[0]), 1);
-    mbar_init(smem_addr(&mbar[1]), 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    mbar_arm(smem_addr(&mbar[0]), C * msgbytes);
-    mbar_arm(smem_addr(&mbar[1]), C * msgbytes);
+    if constexpr (!GX) {
+      mbar_init(smem_addr(&mbar[0]), 1);
+      mbar_init(smem_addr(&mbar[1]), 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      mbar_arm(smem_addr(&mbar[0]), C * msgbytes);
+      mbar_arm(smem_addr(&mbar[1]), C * msgbytes);
+    }
     st->E = E0s;
     st->it = 0;
     st->G = 0;
@@ -440,7 +461,8 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
     st->rb_from = 0;
     st->stop = 0;
   }
-  cluster.sync();
+  if constexpr (GX) __syncthreads();
+  else cg::this_cluster().sync();
 
   const bool prof = P.prof != nullptr && slot == 0 && rank == 0 && tid == 0;
   long long tprev = clock64();
@@ -453,7 +475,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
 
   // warp 0: push the message (top-K records + per-candidate maxima) into slot
   // `slot` of every CTA
-  auto publish = [&](int slot) {
+  auto publish = [&](int ps, unsigned long long stamp) {
     if (lane < K) mymsg->list[lane] = tk[lane] >= 0 ? trec[tk[lane]] : empty_rec(R(0));
     if (lane < BMAX) {
       mymsg->vkey[lane] = vkey[lane];
@@ -463,28 +485,51 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
     PROF_MARK(13);
     const int NCHUNK = (int)(msgbytes / 16);
     const uint4* src = reinterpret_cast<const uint4*>(mymsg);
-    const uint32_t dst = smem_addr(&mail[slot * MAX_CLUSTER + rank]);
-    const uint32_t bar = smem_addr(&mbar[slot]);
-    for (int t = lane; t < C * NCHUNK; t += 32) {
-      const int d = t / NCHUNK, ch = t - d * NCHUNK;
-      st_async16(mapa(dst + 16 * ch, d), mapa(bar, d), src[ch]);
+    if constexpr (GX) {  // message, then its stamp (release): round `stamp - 1` may read it
+      uint4* dstg = reinterpret_cast<uint4*>(reinterpret_cast<MsgT*>(P.gx_rec) + (long long)ps * C + rank);
+      for (int ch = lane; ch < NCHUNK; ch += 32) dstg[ch] = src[ch];
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) gx_st_release(P.gx_stamp + (long long)ps * C + rank, stamp);
+    } else {
+      (void)stamp;
+      const uint32_t dst = smem_addr(&mail[ps * MAX_CLUSTER + rank]);
+      const uint32_t bar = smem_addr(&mbar[ps]);
+      for (int t = lane; t < C * NCHUNK; t += 32) {
+        const int d = t / NCHUNK, ch = t - d * NCHUNK;
+        st_async16(mapa(dst + 16 * ch, d), mapa(bar, d), src[ch]);
+      }
     }
     PROF_MARK(14);
   };
   cta_topk<R, K>(P, lev, trec, tk, lane, warp, NW);
-  if (warp == 0) publish(0);
+  if (warp == 0) publish(0, 1ull);
 
   long long rounds = 0;
   long long tbusy0 = 0;
   for (int round = 0;; ++round) {
     const int par = round & 1;
-    const MsgT* mb = mail + par * MAX_CLUSTER;
+    const MsgT* mb = GX ? mail : mail + par * MAX_CLUSTER;
+    if constexpr (GX) {
+      // every CTA's message of this round (stamp == round + 1): thread c polls CTA c's
+      // stamp, then copies its message into shared memory (L2 loads, L1 bypassed)
+      const unsigned long long want = (unsigned long long)round + 1;
+      const int NCHUNK = (int)(msgbytes / 16);
+      for (int c = tid; c < C; c += blockDim.x) {
+        while (gx_ld_acquire(P.gx_stamp + (long long)par * C + c) != want) {
+        }
+        const uint4* srcg = reinterpret_cast<const uint4*>(reinterpret_cast<const MsgT*>(P.gx_rec) + (long long)par * C + c);
+        uint4* dsts = reinterpret_cast<uint4*>(mail + c);
+        for (int ch = 0; ch < NCHUNK; ++ch) dsts[ch] = __ldcg(srcg + ch);
+      }
+      __syncthreads();
+    }
     // ---- A0/A1 (warp 0): messages of the previous round; verify its candidates
     if (warp == 0) {
-      mbar_wait(smem_addr(&mbar[par]), (uint32_t)((round >> 1) & 1));
+      if constexpr (!GX) mbar_wait(smem_addr(&mbar[par]), (uint32_t)((round >> 1) & 1));
       if (P.prof != nullptr && slot == 0 && tid == 0) tbusy0 = clock64();
       PROF_MARK(0);
-      if (lane == 0) mbar_arm(smem_addr(&mbar[par]), C * msgbytes);  // slot reused at round + 2
+      if (!GX && lane == 0) mbar_arm(smem_addr(&mbar[par]), C * msgbytes);  // slot reused at round + 2
       const int Gp = st->G;
       int acc = Gp;
       if (Gp >= 2) {
@@ -492,13 +537,16 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
         // max_{l<i} V_l < key(c(p_i)) for it and every earlier candidate
         uint32_t vk[BMAX];
 #pragma unroll
-        for (int q = 0; q < BMAX / 4; ++q) {
-          const uint4 va = lane < C ? *reinterpret_cast<const uint4*>(&mb[lane].vkey[4 * q]) : make_uint4(0, 0, 0, 0);
-          vk[4 * q] = va.x;
-          vk[4 * q + 1] = va.y;
-          vk[4 * q + 2] = va.z;
-          vk[4 * q + 3] = va.w;
-        }
+        for (int l = 0; l < BMAX; ++l) vk[l] = 0;
+        for (int c = lane; c < C; c += 32)   // lane: CTAs lane, lane + 32, ... (grid mode)
+#pragma unroll
+          for (int q = 0; q < BMAX / 4; ++q) {
+            const uint4 va = *reinterpret_cast<const uint4*>(&mb[c].vkey[4 * q]);
+            vk[4 * q] = max(vk[4 * q], va.x);
+            vk[4 * q + 1] = max(vk[4 * q + 1], va.y);
+            vk[4 * q + 2] = max(vk[4 * q + 2], va.z);
+            vk[4 * q + 3] = max(vk[4 * q + 3], va.w);
+          }
         uint32_t run = 0;
 #pragma unroll
         for (int l = 0; l < BMAX - 1; ++l) {
@@ -532,7 +580,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
     if (warp != 0 || NW == 1) {
       const bool prof1 = P.prof != nullptr && rank == 0 && tid == 32;
       const long long tw0 = prof1 ? clock64() : 0;
-      if (warp != 0) mbar_wait(smem_addr(&mbar[par]), (uint32_t)((round >> 1) & 1));
+      if (!GX && warp != 0) mbar_wait(smem_addr(&mbar[par]), (uint32_t)((round >> 1) & 1));
       const long long tw1 = prof1 ? clock64() : 0;
       // ---- A2: window ranking, in parallel with the verification: merged position
       //      of every published list entry = the number of entries ahead of it in
@@ -540,7 +588,28 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
       //      4 lanes per entry; the NEc first positions name the walk window
       const int NL = C * K;
       const int rw = NW == 1 ? 0 : warp - 1, nrw = NW == 1 ? 1 : NW - 1;
-      for (int grp = rw; grp * 8 < NL; grp += nrw) {
+      if constexpr (GX) {
+        // stage 1 (C <= 128 heads, 4 lanes per head): the lists whose heads are among
+        // the NEc best heads hold every entry of the window (an entry below the
+        // NEc-th best head has NEc heads ahead of it)
+        for (int grp = rw; grp * 8 < C; grp += nrw) {
+          const int c0 = grp * 8 + (lane >> 2), sub = lane & 3;
+          int cnt = 0;
+          const int ce = c0 < C ? c0 : 0;
+          const uint64_t ke = skey64(mb[ce].list[0].s);
+          const uint32_t pe = mb[ce].list[0].p;
+          for (int f = sub; f < C; f += 4) {
+            const uint64_t kf = skey64(mb[f].list[0].s);
+            const uint32_t pf = mb[f].list[0].p;
+            const bool ahead = (kf > ke) | ((kf == ke) & ((pf < pe) | ((pf == pe) & (f < ce))));
+            cnt += (int)ahead;
+          }
+          cnt += __shfl_xor_sync(0xffffffffu, cnt, 1);
+          cnt += __shfl_xor_sync(0xffffffffu, cnt, 2);
+          if (c0 < C && sub == 0 && cnt < NEc) hsel[cnt] = c0;
+        }
+      }
+      for (int grp = rw; !GX && grp * 8 < NL; grp += nrw) {
         const int e = grp * 8 + (lane >> 2), sub = lane & 3;
         int c = 0;
         if (e < NL) {
@@ -573,8 +642,30 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
     const int mode = st->mode;
     int lo = 0, hi = 0, gvend = 0;  // row-item range of this CTA, number of (g, v) pairs searched
     if (mode == 0) {
+      if constexpr (GX) {
+        // stage 2 (warp 0): the K entries of each selected list, one per lane, ranked
+        // among themselves -- exact, since every entry ahead of one of them is one of them
+        static_assert(NE * K <= 32, "stage-2 candidates fit one warp");
+        if (warp == 0) {
+          const bool have = lane < NEc * K;
+          const int cl = have ? hsel[lane / K] : 0, q = lane % K;
+          const int e = cl * K + q;
+          const uint64_t ke = have ? skey64(mb[cl].list[q].s) : 0ull;
+          const uint32_t pe = have ? mb[cl].list[q].p : NO_INDEX;
+          int cnt = 0;
+#pragma unroll 8
+          for (int j = 0; j < 32; ++j) {
+            const uint64_t kf = __shfl_sync(0xffffffffu, ke, j);
+            const uint32_t pf = __shfl_sync(0xffffffffu, pe, j);
+            const int ef = __shfl_sync(0xffffffffu, e, j);
+            const bool ahead = (kf > ke) | ((kf == ke) & ((pf < pe) | ((pf == pe) & (ef < e))));
+            cnt += (int)((j < NEc * K) & ahead);
+          }
+          if (have && cnt < NEc) sorted[cnt] = e;
+        }
+        __syncthreads();
+      }
       PROF_MARK(3);
-      __syncthreads();
       // ---- A2b: update geometry of every window entry in every target dictionary,
       //      seen from this CTA (Alg. 3 index sets), and its packed tile rect; and,
       //      one thread per window entry, its decoded index and scalar step
@@ -1028,7 +1119,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
     cta_topk<R, K>(P, lev, trec, tk, lane, warp, NW);
     if (P.prof != nullptr && slot == 0 && tid == 0 && rank < 16)  // per-CTA busy time (receive -> publish), slots 40..55
       atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 40 + rank, (unsigned long long)(clock64() - tbusy0));
-    if (warp == 0) publish(par ^ 1);
+    if (warp == 0) publish(par ^ 1, (unsigned long long)round + 2);
   }
   if (rank == 0 && tid == 0) {
     P.result[slot].n_done = st->it;
@@ -1038,24 +1129,29 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
   }
   if (prof) P.prof[15] = rounds;
 #undef PROF_MARK
-  cluster.sync();  // keep every CTA's shared memory alive until all remote stores are done
+  if constexpr (!GX) cg::this_cluster().sync();  // keep shared memory alive until all remote stores are done
 }
 
-template <typename R, int TW, bool SREC, int K>
+template <typename R, int TW, bool SREC, int K, bool GX>
 cudaError_t launch_t(const LoopParams& P, int threads, cudaStream_t st) {
-  auto kfn = mp_multi_kernel<R, TW, SREC, K>;
+  auto kfn = mp_multi_kernel<R, TW, SREC, K, GX>;
   CUDA_OK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem_bytes));
-  if (P.C > 8) CUDA_OK(cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  if (!GX && P.C > 8) CUDA_OK(cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(P.C * std::max(1, P.nslot), 1, 1);   // one cluster per signal
+  cfg.gridDim = dim3(P.C * (GX ? 1 : std::max(1, P.nslot)), 1, 1);   // one cluster per signal
   cfg.blockDim = dim3(threads, 1, 1);
   cfg.dynamicSmemBytes = P.smem_bytes;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = P.C;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
+  if (GX) {  // all CTAs co-resident: they spin on each other's stamps
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+  } else {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = P.C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+  }
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kfn, P);
@@ -1063,7 +1159,7 @@ cudaError_t launch_t(const LoopParams& P, int threads, cudaStream_t st) {
 
 template <typename R, int TW, bool SREC, int K>
 int max_cluster_t(int threads, size_t smem) {
-  auto kfn = mp_multi_kernel<R, TW, SREC, K>;
+  auto kfn = mp_multi_kernel<R, TW, SREC, K, false>;
   if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
       cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
     cudaGetLastError();
@@ -1088,21 +1184,38 @@ int max_cluster_t(int threads, size_t smem) {
   return 0;
 }
 
-template <typename R, bool SREC>
+// co-resident CTAs of the global-exchange kernel (one per SM at most)
+template <typename R, int TW, bool SREC, int K>
+int max_grid_t(int threads, size_t smem) {
+  auto kfn = mp_multi_kernel<R, TW, SREC, K, true>;
+  if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  int per_sm = 0, dev = 0, sms = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, threads, smem) != cudaSuccess ||
+      cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return per_sm * sms;
+}
+
+template <typename R, bool SREC, bool GX>
 cudaError_t launch_r(const LoopParams& P, int threads, cudaStream_t st) {
   switch (P.TW) {
-    case 32: return launch_t<R, 32, SREC, MULTI_K>(P, threads, st);
-    case 64: return launch_t<R, 64, SREC, MULTI_K>(P, threads, st);
-    case 128: return launch_t<R, 128, SREC, MULTI_K>(P, threads, st);
+    case 32: return launch_t<R, 32, SREC, MULTI_K, GX>(P, threads, st);
+    case 64: return launch_t<R, 64, SREC, MULTI_K, GX>(P, threads, st);
+    case 128: return launch_t<R, 128, SREC, MULTI_K, GX>(P, threads, st);
   }
   return cudaErrorInvalidValue;
 }
 template <typename R, bool SREC>
-int max_cluster_r(int TW, int threads, size_t smem) {
+int max_cluster_r(int TW, int threads, size_t smem, bool gx) {
   switch (TW) {
-    case 32: return max_cluster_t<R, 32, SREC, MULTI_K>(threads, smem);
-    case 64: return max_cluster_t<R, 64, SREC, MULTI_K>(threads, smem);
-    case 128: return max_cluster_t<R, 128, SREC, MULTI_K>(threads, smem);
+    case 32: return gx ? max_grid_t<R, 32, SREC, MULTI_K>(threads, smem) : max_cluster_t<R, 32, SREC, MULTI_K>(threads, smem);
+    case 64: return gx ? max_grid_t<R, 64, SREC, MULTI_K>(threads, smem) : max_cluster_t<R, 64, SREC, MULTI_K>(threads, smem);
+    case 128: return gx ? max_grid_t<R, 128, SREC, MULTI_K>(threads, smem) : max_cluster_t<R, 128, SREC, MULTI_K>(threads, smem);
   }
   return 0;
 }
@@ -1117,11 +1230,18 @@ size_t multi_smem_bytes(const LoopParams& P, bool f64) {
 int multi_max_batch() { return BMAX; }
 
 cudaError_t launch_multi_loop(const LoopParams& P, bool f64, int threads, cudaStream_t st) {
-  if (f64) return P.srec ? launch_r<double, true>(P, threads, st) : launch_r<double, false>(P, threads, st);
-  return P.srec ? launch_r<float, true>(P, threads, st) : launch_r<float, false>(P, threads, st);
+  if (P.gx) {
+    if (f64) return P.srec ? launch_r<double, true, true>(P, threads, st) : launch_r<double, false, true>(P, threads, st);
+    return P.srec ? launch_r<float, true, true>(P, threads, st) : launch_r<float, false, true>(P, threads, st);
+  }
+  if (f64) return P.srec ? launch_r<double, true, false>(P, threads, st) : launch_r<double, false, false>(P, threads, st);
+  return P.srec ? launch_r<float, true, false>(P, threads, st) : launch_r<float, false, false>(P, threads, st);
 }
 
-int multi_max_cluster(bool f64, bool srec, int TW, int threads, size_t smem) {
-  if (f64) return srec ? max_cluster_r<double, true>(TW, threads, smem) : max_cluster_r<double, false>(TW, threads, smem);
-  return srec ? max_cluster_r<float, true>(TW, threads, smem) : max_cluster_r<float, false>(TW, threads, smem);
+int multi_max_cluster(bool f64, bool srec, int TW, int threads, size_t smem, bool gx) {
+  if (f64)
+    return srec ? max_cluster_r<double, true>(TW, threads, smem, gx) : max_cluster_r<double, false>(TW, threads, smem, gx);
+  return srec ? max_cluster_r<float, true>(TW, threads, smem, gx) : max_cluster_r<float, false>(TW, threads, smem, gx);
 }
+
+size_t multi_msg_bytes(bool f64) { return f64 ? sizeof(Msg<double, MULTI_K>) : sizeof(Msg<float, MULTI_K>); }

@@ -76,7 +76,7 @@ struct mpgabor {
   int batch = 0;          // candidates per round: 0 auto (multi-selection, multi_max_batch()), 1 one selection
   int kind = 2;           // loop kernel: 0 mploop.cu, 2 mpmulti.cu
   bool force_single = false;  // multi-selection impossible for this layout: use mploop.cu
-  bool gx = false;            // one-selection kernel as a cooperative grid (> 16 CTAs, global exchange)
+  bool gx = false;            // loop kernel as a cooperative grid (> 16 CTAs, global exchange)
   bool batch_mode = false;    // batched signals: one cluster per signal
   int batch_C = 16;           // batched signals: automatic cluster size per signal
   int pedantic = 0;           // 1: pedantic selection (Eq. (20) energies)
@@ -507,10 +507,8 @@ static bool auto_multi(const mpgabor* h, int64_t P_R) {
   const double per_atom = mean_update(h);
   // rounds need independent atoms: small patches relative to the grid (C0's patch
   // covers 2.6 % of its grid and gives ~2 atoms per round)
-  // break-even between C3 (18.6k coefficients per atom: 4.3 vs 5.0 us/atom fp64, 3.6 vs
-  // 4.7 fp32) and C4 (54k: 9.1 vs 7.5 fp64 on a 64-CTA grid)
-  const double limit = 30000.0;
-  return per_atom < limit && per_atom < 0.005 * (double)P_R;
+  // (wide updates run the multi-selection kernel as a grid of 64 / 128 CTAs, below)
+  return per_atom < 0.005 * (double)P_R;
 }
 static bool auto_multi(const mpgabor* h) { return auto_multi(h, h->P_R); }
 
@@ -524,6 +522,7 @@ static size_t plan_loop(mpgabor* h, int TW, int srec, int C) {
   P.Rmax = h->Rmax;
   P.rho_total = h->rho_total;
   P.C = C;
+  P.gx = h->gx ? 1 : 0;
   // frame ownership: global frame f -> CTA f mod C; per (CTA, dictionary) first owned
   // frame, owned-frame count and the local index of the first tile record
   h->own.assign((size_t)C * h->W, OwnGeo{});
@@ -589,13 +588,18 @@ static int ensure_layout(mpgabor* h, int64_t Ls) {
   }
   const bool multi_wanted = !(h->batch == 1 || (h->batch == 0 && !auto_multi(h)));
   // multi-selection: narrow tiles matter more than shared-memory records (C3 fp64: 64-bin
-  // tiles with global records 4.31 us/atom, 128-bin tiles with shared records 6.66)
-  std::vector<Cand> pref;
-  if (h->TW_req) pref = {{h->TW_req, 1}, {h->TW_req, 0}};
-  else if (multi_wanted) pref = {{32, 1}, {64, 1}, {64, 0}, {32, 0}, {128, 1}, {128, 0}};
-  else pref = {{64, 1}, {128, 1}, {64, 0}, {128, 0}};
-  for (const Cand& c : pref)
-    if ((c.srec == 1 && h->srec_req != 2) || (c.srec == 0 && h->srec_req != 1)) cands.push_back(c);
+  // tiles with global records 4.31 us/atom, 128-bin tiles with shared records 6.66); as a
+  // grid of 64 / 128 CTAs (C3 / C4) 64-bin tiles are best
+  auto candidates = [&](bool grid) {
+    std::vector<Cand> pref, out;
+    if (h->TW_req) pref = {{h->TW_req, 1}, {h->TW_req, 0}};
+    else if (multi_wanted && grid) pref = {{64, 1}, {64, 0}, {32, 1}, {32, 0}, {128, 1}, {128, 0}};
+    else if (multi_wanted) pref = {{32, 1}, {64, 1}, {64, 0}, {32, 0}, {128, 1}, {128, 0}};
+    else pref = {{64, 1}, {128, 1}, {64, 0}, {128, 0}};
+    for (const Cand& c : pref)
+      if ((c.srec == 1 && h->srec_req != 2) || (c.srec == 0 && h->srec_req != 1)) out.push_back(c);
+    return out;
+  };
   std::string why = "no candidate";
   bool ok = false;
   // the multi-selection kernel packs tile rects as (row 20 bits, rows 12 bits) and
@@ -605,16 +609,20 @@ static int ensure_layout(mpgabor* h, int64_t Ls) {
     if (L / h->dicts[v].a >= (1 << 20)) h->force_single = true;
   for (int i = 0; i < W * W; ++i)
     if ((h->pairs[i].nnu + h->pairs[i].s_n - 1) / h->pairs[i].s_n >= (1 << 12)) h->force_single = true;
-  // automatic grid mode: very wide updates (C4: ~54k coefficients per atom) spread over 64
-  // CTAs beat one 16-CTA cluster despite the global-memory exchange
-  const bool single = h->batch == 1 || (h->batch == 0 && !auto_multi(h));
-  const bool try_grid = h->cluster_req == 0 && single && mean_update(h) > 30000.0 && !h->batch_mode;
+  // automatic grid mode: wide updates spread over 64 / 128 CTAs beat one 16-CTA cluster
+  // despite the global-memory exchange: multi-selection rounds from ~10k
+  // coefficients per atom (C3: 2.85 vs 4.20 us/atom on 64 CTAs; C4, 54k: 3.93 on 128 CTAs),
+  // the one-selection loop (exchange every atom) from ~30k (C4: 7.5 on 64 CTAs)
+  const double per_atom = mean_update(h);
+  const int grid_C = !multi_wanted ? (per_atom > 30000.0 ? 64 : 0) : (per_atom > 40000.0 ? 128 : (per_atom > 10000.0 ? 64 : 0));
+  const bool try_grid = h->cluster_req == 0 && grid_C > 0 && !h->batch_mode;
   const bool force_single0 = h->force_single;
   for (int pass = try_grid ? 0 : 1; pass < 2 && !ok; ++pass) {
-  int creq = pass == 0 ? 64 : (h->batch_mode && h->cluster_req > MAX_CLUSTER ? 0 : h->cluster_req);
+  int creq = pass == 0 ? grid_C : (h->batch_mode && h->cluster_req > MAX_CLUSTER ? 0 : h->cluster_req);
   if (pass == 1 && h->batch_mode && h->cluster_req == 0) creq = h->batch_C;
   h->gx = creq > MAX_CLUSTER;
-  h->force_single = force_single0 || h->gx;  // grid mode: one-selection kernel
+  h->force_single = force_single0;
+  cands = candidates(h->gx);
   for (int attempt = 0; attempt < 2 && !ok; ++attempt) {
   if (attempt == 1) {
     if (h->kind != 2) break;
@@ -629,7 +637,7 @@ static int ensure_layout(mpgabor* h, int64_t Ls) {
         why = "shared memory " + std::to_string(smem) + " B";
         break;  // smaller clusters need more per-CTA memory
       }
-      const int cmax = h->kind == 2 ? multi_max_cluster(h->f64(), c.srec, c.TW, h->run_threads, smem)
+      const int cmax = h->kind == 2 ? multi_max_cluster(h->f64(), c.srec, c.TW, h->run_threads, smem, h->gx)
                                     : loop_max_cluster(h->f64(), c.srec, c.TW, h->run_threads, smem, h->gx);
       if (cmax >= C) {
         ok = true;
@@ -662,7 +670,9 @@ static int ensure_layout(mpgabor* h, int64_t Ls) {
   TRY_CUDA(h, h->E0.ensure(sizeof(double)));
   TRY_CUDA(h, h->result.ensure(sizeof(LoopResult)));
   if (h->gx) {
-    TRY_CUDA(h, h->gxrec.ensure((h->f64() ? sizeof(Rec<double>) : sizeof(Rec<float>)) * 2 * P.C));
+    // one-selection kernel: [2][C] root records; multi-selection kernel: [2][C] messages
+    TRY_CUDA(h, h->gxrec.ensure(std::max(h->f64() ? sizeof(Rec<double>) : sizeof(Rec<float>), multi_msg_bytes(h->f64())) *
+                                2 * P.C));
     TRY_CUDA(h, h->gxstamp.ensure(sizeof(unsigned long long) * 2 * P.C));
   }
   if (h->kind == 2) {

@@ -275,6 +275,41 @@ def test_grid_mode_bitwise_identical(mpg, name, prec, K):
     mp.close()
 
 
+@pytest.mark.parametrize("name,prec,K", [("C2", "f64", 3000), ("C3", "f64", 3000), ("C4", "f64", 1500),
+                                         ("C4", "f32", 1500)])
+def test_multi_selection_grid_mode_bitwise_identical(mpg, name, prec, K):
+    # the multi-selection loop as a cooperative grid of 32/64/128 CTAs (messages through
+    # global memory, two-stage window ranking) gives the one-selection decomposition, bit
+    # for bit, including roll-backs
+    cfg = CONFIGS[name]
+    x, S = setup_of(name)
+    xd = torch.from_numpy(x).cuda()
+    mp = mpg.MPGabor(cfg.dicts, cfg.thr, prec)
+    mp.set_batch(1)
+    mp.set_launch(16, 0, 0, 0)
+    ref = mp.run(xd, K, cfg.errdb)
+    res_ref = mp.residual(cfg.Ls).cpu().numpy()
+    mp.set_batch(8)
+    for C in (32, 64, 128):
+        mp.set_launch(C, 0, 0, 0)
+        out = mp.run(xd, K, cfg.errdb)
+        assert mp.launch_info()["cluster"] == C and out.rounds < 0.6 * out.n
+        assert out.atoms.tobytes() == ref.atoms.tobytes() and out.energy.tobytes() == ref.energy.tobytes(), C
+        assert np.array_equal(mp.residual(cfg.Ls).cpu().numpy(), res_ref), C
+    mp.close()
+
+
+@pytest.mark.parametrize("name,C", [("C3", 64), ("C4", 128)])
+def test_automatic_grid_multi_selection(mpg, name, C):
+    # wide updates: the automatic choice runs multi-selection rounds on a grid of CTAs
+    cfg = CONFIGS[name]
+    x, S = setup_of(name)
+    mp = mpg.MPGabor(cfg.dicts, cfg.thr, "f64")
+    out = mp.run(torch.from_numpy(x).cuda(), 1000, cfg.errdb)
+    assert mp.launch_info()["cluster"] == C and out.rounds < 0.6 * out.n
+    mp.close()
+
+
 def test_multi_selection_solution_vector(mpg):
     # the solution vector c (Alg. 1 step 2a) only accumulates verified atoms
     cfg = CONFIGS["C1"]
