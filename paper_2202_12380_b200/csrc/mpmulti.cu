@@ -485,12 +485,12 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
     PROF_MARK(13);
     const int NCHUNK = (int)(msgbytes / 16);
     const uint4* src = reinterpret_cast<const uint4*>(mymsg);
-    if constexpr (GX) {  // message, then its stamp (release): round `stamp - 1` may read it
-      uint4* dstg = reinterpret_cast<uint4*>(reinterpret_cast<MsgT*>(P.gx_rec) + (long long)ps * C + rank);
-      for (int ch = lane; ch < NCHUNK; ch += 32) dstg[ch] = src[ch];
-      __threadfence();
-      __syncwarp();
-      if (lane == 0) gx_st_release(P.gx_stamp + (long long)ps * C + rank, stamp);
+    if constexpr (GX) {  // message, then its stamp (release, same thread): round `stamp - 1` may read it
+      if (lane == 0) {
+        uint4* dstg = reinterpret_cast<uint4*>(reinterpret_cast<MsgT*>(P.gx_rec) + (long long)ps * C + rank);
+        for (int ch = 0; ch < NCHUNK; ++ch) dstg[ch] = src[ch];
+        gx_st_release(P.gx_stamp + (long long)ps * C + rank, stamp);
+      }
     } else {
       (void)stamp;
       const uint32_t dst = smem_addr(&mail[ps * MAX_CLUSTER + rank]);
@@ -598,11 +598,13 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
           const int ce = c0 < C ? c0 : 0;
           const uint64_t ke = skey64(mb[ce].list[0].s);
           const uint32_t pe = mb[ce].list[0].p;
-          for (int f = sub; f < C; f += 4) {
-            const uint64_t kf = skey64(mb[f].list[0].s);
-            const uint32_t pf = mb[f].list[0].p;
+#pragma unroll 8
+          for (int f = sub; f < 128; f += 4) {  // C <= 128; every load issued before the compares
+            const int fc = f < C ? f : 0;
+            const uint64_t kf = skey64(mb[fc].list[0].s);
+            const uint32_t pf = mb[fc].list[0].p;
             const bool ahead = (kf > ke) | ((kf == ke) & ((pf < pe) | ((pf == pe) & (f < ce))));
-            cnt += (int)ahead;
+            cnt += (int)(ahead & (f < C));
           }
           cnt += __shfl_xor_sync(0xffffffffu, cnt, 1);
           cnt += __shfl_xor_sync(0xffffffffu, cnt, 2);
