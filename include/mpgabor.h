@@ -178,11 +178,14 @@ int mpgabor_decompose_host(mpgabor* h, const double* x_host, int64_t Ls, int64_t
                            mpg_result* res, void* cuda_stream);
 
 /* Launch tuning of the persistent loop: cluster size (1..16 CTAs, one per SM,
- * power of two; or 32, 64, 128: the one-selection loop as a cooperative grid of
- * that many CTAs exchanging their roots through global memory), threads per CTA (128..512, multiple of 32), tile width in
- * bins (32, 64 or 128), tile-record placement (1 shared memory, 2 global
- * memory).  0 selects automatically (largest cluster; shared records with
- * tile width 64, else 128, else global records).  Takes effect at the next run. */
+ * power of two; or 32, 64, 128: the loop kernel as a cooperative grid of that many
+ * CTAs exchanging their roots / messages through global memory), threads per CTA
+ * (128..512, multiple of 32), tile width in bins (32, 64 or 128), tile-record
+ * placement (1 shared memory, 2 global memory).  0 selects automatically: a 16-CTA
+ * cluster, or a grid of 64 / 128 CTAs for wide updates (multi-selection from ~10k /
+ * 40k coefficients per atom, one selection from 30k); tile width 32 then 64 for the
+ * multi-selection cluster, 64 first for grids and the one-selection loop; shared
+ * records where they fit.  Takes effect at the next run. */
 int mpgabor_set_launch(mpgabor* h, int32_t cluster, int32_t threads, int32_t tile_width, int32_t records);
 
 /* Selection rule (Alg. 1 step 1).  on = 0 (default): argmax |c^|^2 over the reduced
@@ -196,11 +199,10 @@ int mpgabor_set_pedantic(mpgabor* h, int32_t on);
  * atoms are verified against the sequential argmax rule (Alg. 1, ties
  * Z10) and rolled back bit-exactly when the proof fails, so the atom sequence,
  * coefficients and energies are those of the one-selection loop for every value.
- * 0 = automatic: batch 8 when the mean update of an atom is small (< 3000
- * coefficients, estimated from the kernel boxes, and < 0.5 % of the reduced
- * coefficients), else one selection per
- * iteration (DESIGN.md §8 has the measured crossover); 1 = one selection per
- * iteration (the plain persistent loop); 2..8 = that batch.  EINVAL outside
+ * 0 = automatic: batch 8 when an atom's update (estimated from the kernel boxes)
+ * covers < 0.5 % of the reduced coefficients (C1..C4), else one selection per
+ * iteration (C0); DESIGN.md §6b/§6c have the measured crossovers; 1 = one selection
+ * per iteration (the plain persistent loop); 2..8 = that batch.  EINVAL outside
  * [0, 8].  Takes effect at the next run. */
 int mpgabor_set_batch(mpgabor* h, int32_t max_batch);
 /* The launch plan used by the last mpgabor_run (host outputs, may be NULL);
@@ -242,18 +244,21 @@ int mpgabor_residual(mpgabor* h, double* out_dev, void* cuda_stream);
  * (one-selection kernel).  EINVAL outside [0, 3]. */
 int mpgabor_set_profile(mpgabor* h, int32_t mode);
 
-/* cycles (host int64[32]) of the last run with mode bit0, summed over the
+/* cycles (host int64[64]) of the last run with mode bit0, summed over the
  * iterations on CTA 0 / thread 0.  One-selection loop (mpgabor_set_batch 1):
  * [0] wait for the C roots (mailbox barrier), [1] selection + scalar step,
  * [2] block barrier after selection, [3] own update work, [4] block barrier
  * after the update, [5] level-1 refresh + barrier, [6] upper levels + root
  * publication; [7] iterations.  Multi-selection loop: [0] wait for the
- * messages, [1] verification, [2] barrier, [3] list ranking, [4] barrier,
- * [5] window geometry + scalar steps, [6] barrier, [7] pairwise masks,
- * [8] barrier, [9] walk + item bases, [10] barrier, [11] own items,
- * [12] barrier + level-1 refresh + barrier, [13] upper levels + top-K,
- * [14] message push; [15] rounds; [16..19] own items: set-up, loads and
- * update, tile bookkeeping, items processed. */
+ * messages, [1] verification, [2] barrier (window ranking on warps 1..),
+ * [4] window geometry + scalar steps + barrier, [5] pair masks, [6] wait for the
+ * pair warps, [29] walk set-up, [27] walk, [28] E chain + atoms, [9] item bases,
+ * [10] barrier, [11] own items, [12] level refresh + barriers, [13] top-K,
+ * [14] message push; [15] rounds; [16..19] own items: set-up, loads and update,
+ * tile bookkeeping, items processed; [20] sum of the walk's last window position,
+ * [21..26] walk end reasons (window, list exhausted, zero score, overlap, last list
+ * entry); [30], [31] warp 1: wait, ranking; [40..55] CTAs 0..15: busy cycles
+ * (messages received -> message published). */
 int mpgabor_last_profile(const mpgabor* h, int64_t* cycles);
 
 void mpgabor_destroy(mpgabor* h);
