@@ -60,6 +60,12 @@ constexpr int BMAX = MPG_BMAX;  // candidates per round (upper bound; LoopParams
 static_assert(BMAX == 8 || BMAX == 16, "candidate slots: 8 or 16");
 static_assert(NE <= 16, "walk window <= 16 entries");
 constexpr int IPL = BMAX * 16 / 32;  // (candidate, dictionary) item bases per lane
+// tiles per work item (consecutive tiles of one row): 2, or MPG_TPI32 for 32-bin tiles
+#ifndef MPG_TPI32
+#define MPG_TPI32 2
+#endif
+template <int TW>
+__host__ __device__ constexpr int tiles_per_item() { return TW == 32 ? MPG_TPI32 : 2; }
 
 template <typename R, int K>
 struct Msg {              // published by every CTA to every CTA at the end of a round
@@ -371,6 +377,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, NW = blockDim.x >> 5;
   constexpr int LGTW = TW == 32 ? 5 : (TW == 64 ? 6 : 7);
   constexpr int NCH = TW / 32;
+  constexpr int TPI = tiles_per_item<TW>();
   const int NEc = min(NE, C * K);
   const int B = max(1, min(BMAX, P.spec));
 
@@ -691,7 +698,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
             decode_p(r.p, sd, W, u, k, j);
             vgeo<LGTW>(sp[u * W + v], sd[u], sd[v], k, j, rank, C, lgC, gg);
           }
-          const int hp = (gg.Tr + 1) >> 1;   // tile pairs per row; its reciprocal for the items
+          const int hp = (gg.Tr + TPI - 1) / TPI;   // items per row; its reciprocal for the items
           gg.pad = hp > 1 ? (int)(0xFFFFFFFFu / (uint32_t)hp + 1u) : 0;
           egeo[t] = gg;
           rect[t] = pack_rect(gg);
@@ -898,7 +905,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
           if (t < GW && v < W && !P.floor_mode) {
             const VGeo& gg = egeo[st->pick[g] * W + v];
             const int rows = gg.nc > 0 ? gg.cntA + gg.cntB : 0;
-            nrw = rows * ((gg.Tr + 1) >> 1);
+            nrw = rows * ((gg.Tr + TPI - 1) / TPI);
             ntl = rows * gg.Tr;
           }
           r4[q] = nrw;
@@ -987,11 +994,11 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
       const VGeo& gg = egeo[st->pick[g] * W + v];
       const DictGeo& dv = sd[v];
       const int Tr = gg.Tr, t0 = gg.t0, MR = dv.MR;
-      const int hp = (Tr + 1) >> 1;
+      const int hp = (Tr + TPI - 1) / TPI;
       const int it = gi - st->ibase[gv];
       // row among this CTA's rows of (g, v): it / hp by the reciprocal (exact: it * hp < 2^32)
       const int i = hp > 1 ? (int)__umulhi((uint32_t)it, (uint32_t)gg.pad) : it;
-      const int tt = 2 * (it - i * hp);   // first tile of the pair
+      const int tt = TPI * (it - i * hp);   // first tile of the item
       const int r = i < gg.cntA ? gg.rhoA + (i << lgC) : gg.rA + gg.rhoB + ((i - gg.cntA) << lgC);
       int nrow = gg.n0 + r;
       if (nrow >= dv.N) nrow -= dv.N;
@@ -1000,7 +1007,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
       C2* bkrow = backup + ((long long)st->tbase[gv] + (long long)i * Tr) * TW;
       const uint32_t pbase = (uint32_t)dv.off + (uint32_t)nrow * (uint32_t)MR;
       if (mode == 1) {
-        for (int q = 0; q < 2 && tt + q < Tr; ++q) {
+        for (int q = 0; q < TPI && tt + q < Tr; ++q) {
           const int t = t0 + tt + q;
           const C2* bk = bkrow + (long long)(tt + q) * TW;
           C2 cv[NCH];
@@ -1036,10 +1043,10 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
           atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 19, 1ull);
           ta = tn;
         }
-        C2 cv[2][NCH], hd[2][NCH], hc[2][NCH];
-        bool fd[2][NCH], fc[2][NCH], cf[2][NCH];
+        C2 cv[TPI][NCH], hd[TPI][NCH], hc[TPI][NCH];
+        bool fd[TPI][NCH], fc[TPI][NCH], cf[TPI][NCH];
 #pragma unroll
-        for (int q = 0; q < 2; ++q)
+        for (int q = 0; q < TPI; ++q)
 #pragma unroll
           for (int ch = 0; ch < NCH; ++ch) {  // issue every load before any store
             const int bin = (t0 + tt + q) * TW + ch * 32 + lane;
@@ -1055,14 +1062,14 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
           }
         if (g > 0) {  // speculative candidate: keep the tiles for a roll-back
 #pragma unroll
-          for (int q = 0; q < 2; ++q)
+          for (int q = 0; q < TPI; ++q)
 #pragma unroll
             for (int ch = 0; ch < NCH; ++ch)
               if (tt + q < Tr && (t0 + tt + q) * TW + ch * 32 + lane < MR)
                 bkrow[(long long)(tt + q) * TW + ch * 32 + lane] = cv[q][ch];
         }
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
+        for (int q = 0; q < TPI; ++q) {
           if (tt + q >= Tr) break;
           const int t = t0 + tt + q;
           C2 cn[NCH];

@@ -591,13 +591,15 @@ static int ensure_layout(mpgabor* h, int64_t Ls) {
   // tiles with global records 4.31 us/atom, 128-bin tiles with shared records 6.66); as a
   // grid of 64 / 128 CTAs (C3 / C4) 64-bin tiles are best
   auto candidates = [&](bool grid) {
-    std::vector<Cand> pref, out;
-    if (h->TW_req) pref = {{h->TW_req, 1}, {h->TW_req, 0}};
-    else if (multi_wanted && grid) pref = {{64, 1}, {64, 0}, {32, 1}, {32, 0}, {128, 1}, {128, 0}};
-    else if (multi_wanted) pref = {{32, 1}, {64, 1}, {64, 0}, {32, 0}, {128, 1}, {128, 0}};
-    else pref = {{64, 1}, {128, 1}, {64, 0}, {128, 0}};
-    for (const Cand& c : pref)
-      if ((c.srec == 1 && h->srec_req != 2) || (c.srec == 0 && h->srec_req != 1)) out.push_back(c);
+    static const Cand multi_grid[6] = {{64, 1}, {64, 0}, {32, 1}, {32, 0}, {128, 1}, {128, 0}};
+    static const Cand multi_cluster[6] = {{32, 1}, {64, 1}, {64, 0}, {32, 0}, {128, 1}, {128, 0}};
+    static const Cand single[4] = {{64, 1}, {128, 1}, {64, 0}, {128, 0}};
+    const Cand req[2] = {{h->TW_req, 1}, {h->TW_req, 0}};
+    const Cand* pref = h->TW_req ? req : (multi_wanted ? (grid ? multi_grid : multi_cluster) : single);
+    const int n = h->TW_req ? 2 : (multi_wanted ? 6 : 4);
+    std::vector<Cand> out;
+    for (int i = 0; i < n; ++i)
+      if ((pref[i].srec == 1 && h->srec_req != 2) || (pref[i].srec == 0 && h->srec_req != 1)) out.push_back(pref[i]);
     return out;
   };
   std::string why = "no candidate";
