@@ -45,6 +45,7 @@ struct LoopResult {
 };
 
 constexpr int MAX_LEVELS = 6;
+constexpr int MPG_PROF_SLOTS = 320;  // mpgabor_last_profile slots
 constexpr int MAX_CLUSTER = 16;
 constexpr int TOP_SCAN = 256;   // the top node level (<= TOP_SCAN nodes) is scanned by one warp
 

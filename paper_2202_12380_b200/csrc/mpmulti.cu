@@ -495,7 +495,8 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
     if constexpr (GX) {  // message, then its stamp (release, same thread): round `stamp - 1` may read it
       if (lane == 0) {
         uint4* dstg = reinterpret_cast<uint4*>(reinterpret_cast<MsgT*>(P.gx_rec) + (long long)ps * C + rank);
-        for (int ch = 0; ch < NCHUNK; ++ch) dstg[ch] = src[ch];
+#pragma unroll
+        for (int ch = 0; ch < (int)(sizeof(MsgT) / 16); ++ch) dstg[ch] = src[ch];
         gx_st_release(P.gx_stamp + (long long)ps * C + rank, stamp);
       }
     } else {
@@ -521,13 +522,17 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
       // every CTA's message of this round (stamp == round + 1): thread c polls CTA c's
       // stamp, then copies its message into shared memory (L2 loads, L1 bypassed)
       const unsigned long long want = (unsigned long long)round + 1;
-      const int NCHUNK = (int)(msgbytes / 16);
+      constexpr int NCHUNK = (int)(sizeof(MsgT) / 16);
       for (int c = tid; c < C; c += blockDim.x) {
         while (gx_ld_acquire(P.gx_stamp + (long long)par * C + c) != want) {
         }
         const uint4* srcg = reinterpret_cast<const uint4*>(reinterpret_cast<const MsgT*>(P.gx_rec) + (long long)par * C + c);
         uint4* dsts = reinterpret_cast<uint4*>(mail + c);
-        for (int ch = 0; ch < NCHUNK; ++ch) dsts[ch] = __ldcg(srcg + ch);
+        uint4 v[NCHUNK];  // all loads in flight before the stores
+#pragma unroll
+        for (int ch = 0; ch < NCHUNK; ++ch) v[ch] = __ldcg(srcg + ch);
+#pragma unroll
+        for (int ch = 0; ch < NCHUNK; ++ch) dsts[ch] = v[ch];
       }
       __syncthreads();
     }
@@ -1126,8 +1131,14 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
     }
     __syncthreads();
     cta_topk<R, K>(P, lev, trec, tk, lane, warp, NW);
-    if (P.prof != nullptr && slot == 0 && tid == 0 && rank < 16)  // per-CTA busy time (receive -> publish), slots 40..55
-      atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 40 + rank, (unsigned long long)(clock64() - tbusy0));
+    if (P.prof != nullptr && slot == 0 && tid == 0) {  // per-CTA busy time (receive -> publish) and items
+      const unsigned long long busy = (unsigned long long)(clock64() - tbusy0);
+      if (rank < 16) atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 40 + rank, busy);
+      if (rank < 128) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 64 + rank, busy);
+        atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 192 + rank, (unsigned long long)(hi - lo));
+      }
+    }
     if (warp == 0) publish(par ^ 1, (unsigned long long)round + 2);
   }
   if (rank == 0 && tid == 0) {

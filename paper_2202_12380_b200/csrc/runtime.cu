@@ -99,7 +99,7 @@ struct mpgabor {
   int passes = 0;         // passes of the last mpgabor_run_reset
 
   int prof_mode = 0;
-  long long prof_host[64] = {};
+  long long prof_host[MPG_PROF_SLOTS] = {};
   DevBuf prof;
   cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   float t_dgt = 0, t_init = 0, t_loop = 0;
@@ -835,8 +835,8 @@ static int run_impl(mpgabor* h, const double* x_dev, int64_t Ls, int64_t maxit, 
   P.pedantic = h->pedantic;
   P.prof = nullptr;
   if (h->prof_mode & 1) {
-    TRY_CUDA(h, h->prof.ensure(sizeof(long long) * 64));
-    TRY_CUDA(h, cudaMemsetAsync(h->prof.p, 0, sizeof(long long) * 64, st));
+    TRY_CUDA(h, h->prof.ensure(sizeof(long long) * MPG_PROF_SLOTS));
+    TRY_CUDA(h, cudaMemsetAsync(h->prof.p, 0, sizeof(long long) * MPG_PROF_SLOTS, st));
     P.prof = h->prof.as<long long>();
   }
   TRY_CUDA(h, cudaEventRecord(h->ev[3], st));
@@ -859,7 +859,7 @@ static int run_impl(mpgabor* h, const double* x_dev, int64_t Ls, int64_t maxit, 
   TRY_CUDA(h, cudaEventElapsedTime(&h->t_dgt, h->ev[0], h->ev[1]));
   TRY_CUDA(h, cudaEventElapsedTime(&h->t_init, h->ev[1], h->ev[2]));
   TRY_CUDA(h, cudaEventElapsedTime(&h->t_loop, h->ev[3], h->ev[4]));
-  if (P.prof) TRY_CUDA(h, cudaMemcpy(h->prof_host, P.prof, sizeof(long long) * 64, cudaMemcpyDeviceToHost));
+  if (P.prof) TRY_CUDA(h, cudaMemcpy(h->prof_host, P.prof, sizeof(long long) * MPG_PROF_SLOTS, cudaMemcpyDeviceToHost));
   for (int b = 0; b < B; ++b) {
     res[b].n_atoms = lr[b].n_done;
     res[b].L_pad = h->L;
@@ -1008,7 +1008,7 @@ extern "C" int mpgabor_set_profile(mpgabor* h, int32_t mode) {
 
 extern "C" int mpgabor_last_profile(const mpgabor* h, int64_t* cycles) {
   if (!h || !cycles) return MPG_EINVAL;
-  for (int i = 0; i < 64; ++i) cycles[i] = h->prof_host[i];
+  for (int i = 0; i < MPG_PROF_SLOTS; ++i) cycles[i] = h->prof_host[i];
   return MPG_OK;
 }
 

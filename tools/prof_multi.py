@@ -38,7 +38,12 @@ for name in cfgs:
         print(f"   walk split: setup {c[29] / n:.0f} bitmask {c[27] / n:.0f} E+atoms {c[28] / n:.0f} item-scan {c[9] / n:.0f}", flush=True)
         print("   top-K per level (pops / barrier / merge / barrier): " + " | ".join(
             " ".join(f"{c[32 + 4 * L + i] / n:.0f}" for i in range(4)) for L in range(3)), flush=True)
-        print("   per-CTA busy cycles/round (receive -> publish): " + " ".join(f"{c[40 + r] / n:.0f}" for r in range(16)), flush=True)
+        Cn = min(128, mp.launch_info()["cluster"])
+        busy = [c[64 + r] / n for r in range(Cn)]
+        items = [c[192 + r] / n for r in range(Cn)]
+        print(f"   per-CTA busy cycles/round (receive -> publish) over {Cn} CTAs: mean {sum(busy) / Cn:.0f} "
+              f"min {min(busy):.0f} max {max(busy):.0f}; items/round mean {sum(items) / Cn:.2f} "
+              f"min {min(items):.2f} max {max(items):.2f}", flush=True)
         if c[19]:
             print(f"   thread-0 items: {c[19]} ({c[19] / n:.2f}/round) setup {c[16] / c[19]:.0f} loads {c[17] / c[19]:.0f} "
                   f"update+bookkeeping {c[18] / c[19]:.0f} cycles/item", flush=True)
