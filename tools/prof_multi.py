@@ -38,6 +38,8 @@ for name in cfgs:
         print(f"   walk split: setup {c[29] / n:.0f} bitmask {c[27] / n:.0f} E+atoms {c[28] / n:.0f} item-scan {c[9] / n:.0f}", flush=True)
         print("   top-K per level (pops / barrier / merge / barrier): " + " | ".join(
             " ".join(f"{c[32 + 4 * L + i] / n:.0f}" for i in range(4)) for L in range(3)), flush=True)
+        print(f"   roll-back rounds {c[56]} ({100 * c[56] / n:.1f} % of rounds); first rejected candidate 1..7: "
+              + " ".join(str(c[56 + i]) for i in range(1, 8)), flush=True)
         Cn = min(128, mp.launch_info()["cluster"])
         busy = [c[64 + r] / n for r in range(Cn)]
         items = [c[192 + r] / n for r in range(Cn)]
