@@ -265,7 +265,6 @@ __device__ __forceinline__ void cta_topk(const LoopParams& P, const Rec<R>* lev,
     const int count = l >= 0 ? P.lev_n[l] : (int)P.Lc;
     const Rec<R>* arr = l >= 0 ? lev + P.lev_off[l] : trec;
     const int nq = first ? (count + 31) >> 5 : K;
-#ifndef MPG_TOPK_CHUNKS
     if (nq <= 4) {  // <= 128 candidates: warp 0 alone, 4 per lane (the other warps wait)
       if (warp == 0) {
         uint64_t kk[4];
@@ -291,7 +290,6 @@ __device__ __forceinline__ void cta_topk(const LoopParams& P, const Rec<R>* lev,
       if (l == -1) __syncthreads();
       continue;
     }
-#endif
     for (int q = warp; q < nq; q += NW) {  // chunk q (fewer warps than chunks: several each)
       int id = first ? q * 32 + lane : (tk[q] >= 0 ? tk[q] * 32 + lane : -1);
       uint64_t key = 0;
