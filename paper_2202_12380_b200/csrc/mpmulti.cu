@@ -68,6 +68,10 @@ constexpr int IPL = BMAX * 16 / 32;  // (candidate, dictionary) item bases per l
 #endif
 template <int TW>
 __host__ __device__ constexpr int tiles_per_item() { return TW == 32 ? MPG_TPI32 : 2; }
+// update items in flight per warp for 32-bin tiles (1 or 2)
+#ifndef MPG_ITEMS_IN_FLIGHT
+#define MPG_ITEMS_IN_FLIGHT 1
+#endif
 
 template <typename R, int K>
 struct Msg {              // published by every CTA to every CTA at the end of a round
@@ -986,25 +990,35 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
         if (atomicExch(&stamp[node], stampv) != stampv) list[atomicAdd(&cnt[0], 1)] = node;
       }
     };
-    for (int gi = lo + warp; gi < hi; gi += NW) {
-      long long ta = prof ? clock64() : 0;
-      // (g, v) of item gi: count the item bases <= gi (ibase is non-decreasing)
-      int gv;
-      {
-        int c = 0;
+    // (g, v) of item gi: count the item bases <= gi (ibase is non-decreasing)
+    auto item_gv = [&](int gi) {
+      int c = 0;
 #pragma unroll
-        for (int h4 = 0; h4 < IPL / 4; ++h4) {
-          const int i0 = lane * IPL + 4 * h4;
-          const int4 b4 = *reinterpret_cast<const int4*>(&st->ibase[i0]);
-          c += (i0 + 0 >= 1 && i0 + 0 <= gvend && b4.x <= gi) ? 1 : 0;
-          c += (i0 + 1 >= 1 && i0 + 1 <= gvend && b4.y <= gi) ? 1 : 0;
-          c += (i0 + 2 <= gvend && b4.z <= gi) ? 1 : 0;
-          c += (i0 + 3 <= gvend && b4.w <= gi) ? 1 : 0;
-        }
-        gv = (int)__reduce_add_sync(0xffffffffu, (unsigned)c);
+      for (int h4 = 0; h4 < IPL / 4; ++h4) {
+        const int i0 = lane * IPL + 4 * h4;
+        const int4 b4 = *reinterpret_cast<const int4*>(&st->ibase[i0]);
+        c += (i0 + 0 >= 1 && i0 + 0 <= gvend && b4.x <= gi) ? 1 : 0;
+        c += (i0 + 1 >= 1 && i0 + 1 <= gvend && b4.y <= gi) ? 1 : 0;
+        c += (i0 + 2 <= gvend && b4.z <= gi) ? 1 : 0;
+        c += (i0 + 3 <= gvend && b4.w <= gi) ? 1 : 0;
       }
+      return (int)__reduce_add_sync(0xffffffffu, (unsigned)c);
+    };
+    // one update item in flight: geometry, then every load issued (setup), then the
+    // fold-rule update, stores and tile bookkeeping (process)
+    struct ItemS {
+      C2* row;
+      C2* bkrow;
+      uint32_t pbase;
+      int l0, t0, tt, Tr, MR, g, v;
+      C2 cv[TPI][NCH], hd[TPI][NCH], hc[TPI][NCH], z0;
+      bool fd[TPI][NCH], fc[TPI][NCH], cf[TPI][NCH];
+    };
+    auto setup = [&](int gi, ItemS& S) {
+      const int gv = item_gv(gi);
       const int g = gv >> 4, v = gv & 15;
-      const VGeo& gg = egeo[st->pick[g] * W + v];
+      const int e = st->pick[g];
+      const VGeo& gg = egeo[e * W + v];
       const DictGeo& dv = sd[v];
       const int Tr = gg.Tr, t0 = gg.t0, MR = dv.MR;
       const int hp = (Tr + TPI - 1) / TPI;
@@ -1015,11 +1029,105 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
       const int r = i < gg.cntA ? gg.rhoA + (i << lgC) : gg.rA + gg.rhoB + ((i - gg.cntA) << lgC);
       int nrow = gg.n0 + r;
       if (nrow >= dv.N) nrow -= dv.N;
-      const int l0 = sown[v].loc_base + ((nrow - sown[v].n_first) >> lgC) * dv.T;
-      C2* row = grid + dv.grid_off + (long long)nrow * dv.stride;
-      C2* bkrow = backup + ((long long)st->tbase[gv] + (long long)i * Tr) * TW;
-      const uint32_t pbase = (uint32_t)dv.off + (uint32_t)nrow * (uint32_t)MR;
-      if (mode == 1) {
+      S.l0 = sown[v].loc_base + ((nrow - sown[v].n_first) >> lgC) * dv.T;
+      S.row = grid + dv.grid_off + (long long)nrow * dv.stride;
+      S.bkrow = backup + ((long long)st->tbase[gv] + (long long)i * Tr) * TW;
+      S.pbase = (uint32_t)dv.off + (uint32_t)nrow * (uint32_t)MR;
+      S.t0 = t0;
+      S.tt = tt;
+      S.Tr = Tr;
+      S.MR = MR;
+      S.g = g;
+      S.v = v;
+      const Ent& en = ent[e];
+      const PairGeo& pg = sp[en.u * W + v];
+      const bool selfc = en.selfc != 0;
+      // modulation omega_R^{(k' nu) mod R} of this row (Eq. (15))
+      const int rrx = (gg.rr0 + r * gg.rrstep) & (pg.R - 1);
+      S.z0 = row_z0<C2, R>(en.tre, en.tim, roots[rrx * pg.rstep]);
+      const C2* hrow = kern + gg.kbase + (long long)r * gg.nc;
+      const int q0 = gg.q0, nc = gg.nc, Mv = dv.M;
+#pragma unroll
+      for (int q = 0; q < TPI; ++q)
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) {  // issue every load before any store
+          const int bin = (t0 + tt + q) * TW + ch * 32 + lane;
+          const bool valid = (tt + q < Tr) && bin < MR;
+          const int cd = (bin - q0) & (Mv - 1);   // direct source column  (q = bin)
+          const int cc = (-bin - q0) & (Mv - 1);  // conjugate source column (q = M - bin)
+          S.fd[q][ch] = valid && cd < nc;
+          S.fc[q][ch] = valid && !selfc && cc < nc;
+          S.cf[q][ch] = cc < cd;                  // oracle order: ascending source column
+          S.cv[q][ch] = valid ? S.row[bin] : C2{0, 0};
+          S.hd[q][ch] = S.fd[q][ch] ? hrow[cd] : C2{0, 0};
+          S.hc[q][ch] = S.fc[q][ch] ? hrow[cc] : C2{0, 0};
+        }
+    };
+    auto process = [&](ItemS& S) {
+      if (S.g > 0) {  // speculative candidate: keep the tiles for a roll-back
+#pragma unroll
+        for (int q = 0; q < TPI; ++q)
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch)
+            if (S.tt + q < S.Tr && (S.t0 + S.tt + q) * TW + ch * 32 + lane < S.MR)
+              S.bkrow[(long long)(S.tt + q) * TW + ch * 32 + lane] = S.cv[q][ch];
+      }
+      const DictGeo& dv = sd[S.v];
+#pragma unroll
+      for (int q = 0; q < TPI; ++q) {
+        if (S.tt + q >= S.Tr) break;
+        const int t = S.t0 + S.tt + q;
+        C2 cn[NCH];
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) {
+          const int bin = t * TW + ch * 32 + lane;
+          cn[ch] = fold_update<R>(S.cv[q][ch], S.z0, S.hd[q][ch], S.hc[q][ch], S.fd[q][ch], S.fc[q][ch], S.cf[q][ch]);
+          if (bin < S.MR && (S.fd[q][ch] || S.fc[q][ch])) S.row[bin] = cn[ch];
+        }
+        R bs, bre, bim;
+        uint32_t bp;
+        lane_best<R, C2, NCH>(cn, t * TW + lane, S.MR, dv.M, S.pbase, P.pedantic != 0, srho + rho_off[S.v],
+                              rho_lo[S.v], rho_n[S.v], bs, bp, bre, bim);
+        finish(S.l0 + t, S.g, bs, bp, bre, bim);
+      }
+    };
+    if (mode == 0) {
+      // MPG_ITEMS_IN_FLIGHT = 2: two items per warp in flight (32-bin tiles only; it spills
+      // at 128 registers and was slower: C2 2.24 vs 1.93 us/atom)
+      constexpr int IF = NCH == 1 ? MPG_ITEMS_IN_FLIGHT : 1;
+      for (int gi = lo + warp; gi < hi; gi += IF * NW) {
+        if constexpr (IF == 2) {
+          ItemS A, B;
+          const bool hasB = gi + NW < hi;
+          setup(gi, A);
+          if (hasB) setup(gi + NW, B);
+          process(A);
+          if (hasB) process(B);
+        } else {
+          ItemS A;
+          setup(gi, A);
+          process(A);
+        }
+      }
+    } else {
+      // roll back the rejected candidates' tiles from their backups
+      for (int gi = lo + warp; gi < hi; gi += NW) {
+        const int gv = item_gv(gi);
+        const int g = gv >> 4, v = gv & 15;
+        const VGeo& gg = egeo[st->pick[g] * W + v];
+        const DictGeo& dv = sd[v];
+        const int Tr = gg.Tr, t0 = gg.t0, MR = dv.MR;
+        const int hp = (Tr + TPI - 1) / TPI;
+        const int it = gi - st->ibase[gv];
+        const int i = hp > 1 ? (int)__umulhi((uint32_t)it, (uint32_t)gg.pad) : it;
+        const int tt = TPI * (it - i * hp);
+        const int r = i < gg.cntA ? gg.rhoA + (i << lgC) : gg.rA + gg.rhoB + ((i - gg.cntA) << lgC);
+        int nrow = gg.n0 + r;
+        if (nrow >= dv.N) nrow -= dv.N;
+        const int l0 = sown[v].loc_base + ((nrow - sown[v].n_first) >> lgC) * dv.T;
+        C2* row = grid + dv.grid_off + (long long)nrow * dv.stride;
+        const C2* bkrow = backup + ((long long)st->tbase[gv] + (long long)i * Tr) * TW;
+        const uint32_t pbase = (uint32_t)dv.off + (uint32_t)nrow * (uint32_t)MR;
         for (int q = 0; q < TPI && tt + q < Tr; ++q) {
           const int t = t0 + tt + q;
           const C2* bk = bkrow + (long long)(tt + q) * TW;
@@ -1039,73 +1147,6 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
           lane_best<R, C2, NCH>(cv, t * TW + lane, MR, dv.M, pbase, P.pedantic != 0, srho + rho_off[v], rho_lo[v],
                                 rho_n[v], bs, bp, bre, bim);
           finish(l0 + t, g, bs, bp, bre, bim);
-        }
-      } else {
-        const Ent& en = ent[st->pick[g]];
-        const PairGeo& pg = sp[en.u * W + v];
-        const bool selfc = en.selfc != 0;
-        // modulation omega_R^{(k' nu) mod R} of this row (Eq. (15))
-        const int rrx = (gg.rr0 + r * gg.rrstep) & (pg.R - 1);
-        const double2 w = roots[rrx * pg.rstep];
-        const C2 z0 = row_z0<C2, R>(en.tre, en.tim, w);
-        const C2* hrow = kern + gg.kbase + (long long)r * gg.nc;
-        const int q0 = gg.q0, nc = gg.nc, Mv = dv.M;
-        if (prof) {
-          const long long tn = clock64();
-          atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 16, (unsigned long long)(tn - ta));
-          atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 19, 1ull);
-          ta = tn;
-        }
-        C2 cv[TPI][NCH], hd[TPI][NCH], hc[TPI][NCH];
-        bool fd[TPI][NCH], fc[TPI][NCH], cf[TPI][NCH];
-#pragma unroll
-        for (int q = 0; q < TPI; ++q)
-#pragma unroll
-          for (int ch = 0; ch < NCH; ++ch) {  // issue every load before any store
-            const int bin = (t0 + tt + q) * TW + ch * 32 + lane;
-            const bool valid = (tt + q < Tr) && bin < MR;
-            const int cd = (bin - q0) & (Mv - 1);   // direct source column  (q = bin)
-            const int cc = (-bin - q0) & (Mv - 1);  // conjugate source column (q = M - bin)
-            fd[q][ch] = valid && cd < nc;
-            fc[q][ch] = valid && !selfc && cc < nc;
-            cf[q][ch] = cc < cd;                    // oracle order: ascending source column
-            cv[q][ch] = valid ? row[bin] : C2{0, 0};
-            hd[q][ch] = fd[q][ch] ? hrow[cd] : C2{0, 0};
-            hc[q][ch] = fc[q][ch] ? hrow[cc] : C2{0, 0};
-          }
-        if (g > 0) {  // speculative candidate: keep the tiles for a roll-back
-#pragma unroll
-          for (int q = 0; q < TPI; ++q)
-#pragma unroll
-            for (int ch = 0; ch < NCH; ++ch)
-              if (tt + q < Tr && (t0 + tt + q) * TW + ch * 32 + lane < MR)
-                bkrow[(long long)(tt + q) * TW + ch * 32 + lane] = cv[q][ch];
-        }
-#pragma unroll
-        for (int q = 0; q < TPI; ++q) {
-          if (tt + q >= Tr) break;
-          const int t = t0 + tt + q;
-          C2 cn[NCH];
-#pragma unroll
-          for (int ch = 0; ch < NCH; ++ch) {
-            const int bin = t * TW + ch * 32 + lane;
-            if (prof && ch == 0 && q == 0) {  // first use of the loaded tile
-              const long long tn = clock64();
-              atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 17, (unsigned long long)(tn - ta));
-              ta = tn;
-            }
-            cn[ch] = fold_update<R>(cv[q][ch], z0, hd[q][ch], hc[q][ch], fd[q][ch], fc[q][ch], cf[q][ch]);
-            if (bin < MR && (fd[q][ch] || fc[q][ch])) row[bin] = cn[ch];
-          }
-          R bs, bre, bim;
-          uint32_t bp;
-          lane_best<R, C2, NCH>(cn, t * TW + lane, MR, dv.M, pbase, P.pedantic != 0, srho + rho_off[v], rho_lo[v],
-                                rho_n[v], bs, bp, bre, bim);
-          finish(l0 + t, g, bs, bp, bre, bim);
-        }
-        if (prof) {
-          const long long tn = clock64();
-          atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 18, (unsigned long long)(tn - ta));
         }
       }
     }
