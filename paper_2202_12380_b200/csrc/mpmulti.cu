@@ -43,6 +43,7 @@
 // are those of mploop.cu; the run is deterministic and its atom sequence is
 // identical to the one-selection loop.
 #include <cooperative_groups.h>
+#include <type_traits>
 #include "loopcore.cuh"
 
 namespace cg = cooperative_groups;
@@ -976,7 +977,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
     // ---- B. residual update (or roll-back) over this CTA's rows ------------
     // tile bookkeeping: record, candidate maximum, dirty level-0 node (stamp + list)
     const int stampv = round + 1;
-    auto finish = [&](int l, int g, R bs, uint32_t bp, R bre, R bim) {
+    auto finish = [&](int l, int g, R bs, uint32_t bp, R bre, R bim, auto upd) {
       if (lane == warp_argmax_lane(bs, bp)) {
         RecT rec;
         rec.s = bs;
@@ -985,7 +986,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
         rec.p = bp;
         if constexpr (sizeof(R) == 8) rec.pad = 0;
         trec[l] = rec;
-        if (mode == 0) atomicMax(&vkey[g], score_key(bs));
+        if constexpr (decltype(upd)::value) atomicMax(&vkey[g], score_key(bs));
         const int node = l >> 5;
         if (atomicExch(&stamp[node], stampv) != stampv) list[atomicAdd(&cnt[0], 1)] = node;
       }
@@ -1088,7 +1089,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
         uint32_t bp;
         lane_best<R, C2, NCH>(cn, t * TW + lane, S.MR, dv.M, S.pbase, P.pedantic != 0, srho + rho_off[S.v],
                               rho_lo[S.v], rho_n[S.v], bs, bp, bre, bim);
-        finish(S.l0 + t, S.g, bs, bp, bre, bim);
+        finish(S.l0 + t, S.g, bs, bp, bre, bim, std::true_type{});
       }
     };
     if (mode == 0) {
@@ -1146,7 +1147,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
           uint32_t bp;
           lane_best<R, C2, NCH>(cv, t * TW + lane, MR, dv.M, pbase, P.pedantic != 0, srho + rho_off[v], rho_lo[v],
                                 rho_n[v], bs, bp, bre, bim);
-          finish(l0 + t, g, bs, bp, bre, bim);
+          finish(l0 + t, g, bs, bp, bre, bim, std::false_type{});
         }
       }
     }
@@ -1154,16 +1155,34 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
     __syncthreads();
     // ---- C. level-0 refresh of the dirty nodes, then the upper levels, one level
     //      at a time, nodes spread over the warps
-    for (int l = 0; l < P.nlev; ++l) {
-      const int nl = cnt[l];
-      const RecT* child = l == 0 ? trec : lev + P.lev_off[l - 1];
-      const long long nchild = l == 0 ? P.Lc : (long long)P.lev_n[l - 1];
+    {  // level 0 (children: the tile records)
+      const int nl = cnt[0];
+      const bool up = P.nlev > 1;
       for (int idx = warp; idx < nl; idx += NW) {
-        const int node = list[(l == 0 ? 0 : P.lev_off[l]) + idx];
+        const int node = list[idx];
+        const long long c = (long long)node * 32 + lane;
+        const RecT rc = c < P.Lc ? trec[c] : empty_rec(R(0));
+        if (lane == warp_argmax_lane(rc.s, rc.p)) {
+          lev[node] = rc;
+          if (up) {
+            const int par2 = node >> 5;
+            int* st2 = stamp + P.lev_off[1];
+            if (atomicExch(&st2[par2], stampv) != stampv) list[P.lev_off[1] + atomicAdd(&cnt[1], 1)] = par2;
+          }
+        }
+      }
+      __syncthreads();
+    }
+    for (int l = 1; l < P.nlev; ++l) {
+      const int nl = cnt[l];
+      const RecT* child = lev + P.lev_off[l - 1];
+      const long long nchild = (long long)P.lev_n[l - 1];
+      for (int idx = warp; idx < nl; idx += NW) {
+        const int node = list[P.lev_off[l] + idx];
         const long long c = (long long)node * 32 + lane;
         const RecT rc = c < nchild ? child[c] : empty_rec(R(0));
         if (lane == warp_argmax_lane(rc.s, rc.p)) {
-          lev[(l == 0 ? 0 : P.lev_off[l]) + node] = rc;
+          lev[P.lev_off[l] + node] = rc;
           if (l + 1 < P.nlev) {
             const int par2 = node >> 5;
             int* st2 = stamp + P.lev_off[l + 1];
