@@ -694,7 +694,11 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
       //      one thread per window entry, its decoded index and scalar step
       //      (c~, E~ of Eqs. (19)-(20): c(p) of an entry that is picked is unchanged
       //      by the round's earlier picks, so they are the sequential ones)
-      for (int t = tid; t < NEc * W + NEc; t += blockDim.x) {
+      // the scalar steps run on their own warp (no divergence with the geometry threads)
+      const int sbase = (NEc * W + 31) & ~31;
+      const int nwork = sbase + NEc <= (int)blockDim.x ? sbase + NEc : NEc * W + NEc;
+      for (int t = tid; t < nwork; t += blockDim.x) {
+        if (nwork == sbase + NEc && t >= NEc * W && t < sbase) continue;
         if (t < NEc * W) {
           const int e = t / W, v = t - e * W;
           const int src = sorted[e];
@@ -717,7 +721,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
           egeo[t] = gg;
           rect[t] = pack_rect(gg);
         } else {
-          const int e = t - NEc * W;
+          const int e = t - (nwork == sbase + NEc ? sbase : NEc * W);
           const int src = sorted[e];
           const RecT rl = mb[src / K].list[src % K];
           Ent en;
