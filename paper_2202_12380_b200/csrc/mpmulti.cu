@@ -105,7 +105,7 @@ struct St {               // round state (shared memory)
 };
 
 struct Smem {
-  size_t mbar, mail, mymsg, trec, lev, ent, egeo, wmask, rect, st, vkey, sorted, hsel, tk, stamp, list, cnt, pairs, dicts, own, roots,
+  size_t mbar, mail, mymsg, trec, lev, ent, egeo, wmask, rect, ecnt, st, vkey, sorted, hsel, tk, stamp, list, cnt, pairs, dicts, own, roots,
       rho, rho_meta, total;
 };
 
@@ -139,6 +139,9 @@ __host__ __device__ inline Smem smem_layout(const LoopParams& P, size_t recsz, s
   o = align_up(o, 16);
   s.rect = o;
   o += sizeof(uint2) * NE * P.W;
+  o = align_up(o, 16);
+  s.ecnt = o;                 // per (window entry, dictionary): this CTA's items and tiles
+  o += sizeof(int2) * NE * 16;
   o = align_up(o, 16);
   s.st = o;
   o += sizeof(St);
@@ -397,6 +400,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
   uint32_t* wmeet = reinterpret_cast<uint32_t*>(smem + L.wmask);
   uint32_t* wcover = wmeet + NE;
   uint2* rect = reinterpret_cast<uint2*>(smem + L.rect);
+  int2* ecnt = reinterpret_cast<int2*>(smem + L.ecnt);
   St* st = reinterpret_cast<St*>(smem + L.st);
   uint32_t* vkey = reinterpret_cast<uint32_t*>(smem + L.vkey);
   int* sorted = reinterpret_cast<int*>(smem + L.sorted);
@@ -720,6 +724,8 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
           gg.pad = hp > 1 ? (int)(0xFFFFFFFFu / (uint32_t)hp + 1u) : 0;
           egeo[t] = gg;
           rect[t] = pack_rect(gg);
+          const int rows = gg.nc > 0 ? gg.cntA + gg.cntB : 0;
+          ecnt[e * 16 + v] = make_int2(rows * hp, rows * gg.Tr);
         } else {
           const int e = t - (nwork == sbase + NEc ? sbase : NEc * W);
           const int src = sorted[e];
@@ -919,16 +925,17 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
         // t = g * 16 + v (g-major; v >= W contribute nothing): lane handles IPL pairs
         const int GW = G * 16;
         int r4[IPL], t4[IPL], rs = 0, ts = 0;
+        // a lane's IPL entries share one candidate g (16 % IPL == 0): its window position
+        const int pq = __shfl_sync(0xffffffffu, pl, ((lane * IPL) >> 4) & 31);
 #pragma unroll
         for (int q = 0; q < IPL; ++q) {
           const int t = lane * IPL + q;
           int nrw = 0, ntl = 0;
-          const int g = t >> 4, v = t & 15;
+          const int v = t & 15;
           if (t < GW && v < W && !P.floor_mode) {
-            const VGeo& gg = egeo[st->pick[g] * W + v];
-            const int rows = gg.nc > 0 ? gg.cntA + gg.cntB : 0;
-            nrw = rows * ((gg.Tr + TPI - 1) / TPI);
-            ntl = rows * gg.Tr;
+            const int2 cn2 = ecnt[pq * 16 + v];
+            nrw = cn2.x;
+            ntl = cn2.y;
           }
           r4[q] = nrw;
           t4[q] = ntl;
