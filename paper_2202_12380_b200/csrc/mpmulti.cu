@@ -739,6 +739,8 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
           en.Et = 0.0;
           en.selfc = 0;
           en.key = score_key(rl.s);
+          en.pos = (rl.p != NO_INDEX && rl.s > R(0)) ? 1 : 0;
+          en.last = (src % K) == K - 1 ? 1 : 0;   // the K-th entry of its CTA's list
           if (rl.p != NO_INDEX) {
             decode_p(rl.p, sd, W, en.u, en.k, en.j);
             const int u = en.u, k = en.k;
@@ -811,15 +813,14 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
       //      meanwhile compute every window entry's update geometry seen from this CTA
       if (warp == 0) {
         const bool have = lane < NEc;
-        const int src = have ? sorted[lane] : 0;
-        const RecT rl = have ? mb[src / K].list[src % K] : empty_rec(R(0));
-        const unsigned lastm = __ballot_sync(0xffffffffu, have && (src % K) == K - 1);
-        const unsigned posm = __ballot_sync(0xffffffffu, have && rl.p != NO_INDEX && rl.s > R(0));
+        const Ent& el = ent[have ? lane : 0];   // decoded in the geometry phase
+        const unsigned lastm = __ballot_sync(0xffffffffu, have && el.last != 0);
+        const unsigned posm = __ballot_sync(0xffffffffu, have && el.pos != 0);
         const long long it0 = st->it;
         const long long rem = P.maxit - it0;
         const int Bm = rem < (long long)B ? (int)max(rem, 0LL) : B;
-        const double Etl = lane < NEc ? ent[lane].Et : 0.0;
-        const uint32_t keyl = lane < NEc ? ent[lane].key : 0u;
+        const double Etl = have ? el.Et : 0.0;
+        const uint32_t keyl = have ? el.key : 0u;
         uint32_t mtr[NE], cvr[NE];  // every entry's masks in every lane (broadcast loads)
 #pragma unroll
         for (int j = 0; j < NE; ++j) {
