@@ -1205,11 +1205,12 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
       __syncthreads();
     }
     PROF_MARK(12);
+    // (no barrier needed: every use of cnt ended at the refresh's last barrier, and
+    // st->G is next read by this thread's warp after the message exchange)
     if (tid == 0) {
       for (int l = 0; l < P.nlev; ++l) cnt[l] = 0;
       if (mode == 1) st->G = 0;  // nothing to verify after a roll-back
     }
-    __syncthreads();
     cta_topk<R, K>(P, lev, trec, tk, lane, warp, NW);
     if (P.prof != nullptr && slot == 0 && tid == 0) {  // per-CTA busy time (receive -> publish) and items
       const unsigned long long busy = (unsigned long long)(clock64() - tbusy0);
