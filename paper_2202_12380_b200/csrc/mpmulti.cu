@@ -23,7 +23,8 @@
 //   inside X_i every value is smaller.  c(p_i) is unchanged by the earlier
 //   updates (p_i is outside X_i), so c~ and E~ (Eqs. (19)-(20)) are the
 //   sequential ones.  The comparison uses a conservative 32-bit score key
-//   (equality rejects), so a rejection never breaks exactness.
+//   (equality rejects): it can only cause spurious rejections, never a wrong
+//   acceptance.
 //   Rejected candidates are rolled back bit-exactly in the next round from a
 //   backup of their tiles (a copy, not an inverse update), and that round does
 //   no selection.
@@ -31,7 +32,8 @@
 // The candidates come from per-CTA top-K lists: at the end of a round every CTA
 // extracts its K best tile records (exact, from its 32-ary max tree) and pushes
 // them, with its per-candidate maxima, into every CTA's mailbox (st.async +
-// mbarrier complete_tx, as in mploop.cu).  Every CTA then runs the same
+// mbarrier complete_tx, as in mploop.cu; in grid mode into global memory with a
+// release stamp, see the kernel).  Every CTA then runs the same
 // deterministic merge/walk: entries in descending (score, -index) order; an
 // entry whose tile lies in X is skipped; passing the K-th entry of a CTA's list
 // ends the walk (that CTA's unlisted tiles are unknown); the walk also ends at
