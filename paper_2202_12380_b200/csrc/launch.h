@@ -88,6 +88,7 @@ struct LoopParams {
   int nslot;                     //   signals (clusters) of the launch
   int pedantic;                  // 1: select by the Eq. (20) energy (pedantic), else |c|^2
   int spec;                      // multi-selection: candidates per round (1..multi_max_batch())
+  int topk_scan;                 // multi-selection: top-K by a scan of the tile records (no node tree upkeep)
   void* backup;                  // multi-selection: per-CTA tile backups [C][bk_cap][TW] (cplx<R>)
   long long bk_cap;              // items per CTA per round the backup holds
   size_t smem_bytes;

@@ -106,8 +106,14 @@ struct St {               // round state (shared memory)
   alignas(16) int tbase[BMAX * 16 + 4];  // this CTA's tiles (backup slots) before (g, v)
 };
 
+struct TkE {              // a top-K candidate: order key, index, id (tile; -1 = none)
+  uint64_t key;
+  uint32_t p;
+  int id;
+};
+
 struct Smem {
-  size_t mbar, mail, mymsg, trec, lev, ent, egeo, wmask, rect, ecnt, st, vkey, sorted, hsel, tk, stamp, list, cnt, pairs, dicts, own, roots,
+  size_t mbar, mail, mymsg, trec, lev, ent, egeo, wmask, rect, ecnt, st, vkey, sorted, hsel, tk, wk, stamp, list, cnt, pairs, dicts, own, roots,
       rho, rho_meta, total;
 };
 
@@ -156,6 +162,9 @@ __host__ __device__ inline Smem smem_layout(const LoopParams& P, size_t recsz, s
   o += sizeof(int) * NE;
   s.tk = o;
   o += sizeof(int) * 64;
+  o = align_up(o, 16);
+  s.wk = o;                   // scan top-K: warp winners (<= 16 warps x K) + the final K
+  o += sizeof(TkE) * (64 + MULTI_K);
   s.stamp = o;
   o += sizeof(int) * levtot;
   s.list = o;
@@ -328,6 +337,107 @@ __device__ __forceinline__ void cta_topk(const LoopParams& P, const Rec<R>* lev,
   }
 }
 
+// Exact top-K tiles of this CTA by a scan of all its tile records (records in shared
+// memory, small slices): every lane keeps its K best of a strided share in a sorted
+// register list (branch-free insertion), each warp pops its K best lane heads, warp 0
+// pops the K best of the NW warps' lists.  No node tree is needed (the caller skips
+// its upkeep).  Leaves the tile ids (-1 = none) in tk[0..K-1]; ends with a barrier.
+template <typename R, int K>
+__device__ __forceinline__ void cta_topk_scan(const Rec<R>* trec, long long Lc, int* tk, TkE* wk, int lane, int warp,
+                                              int NW) {
+  static_assert(K == 4, "sorted 4-lists");
+  uint64_t k[4] = {0ull, 0ull, 0ull, 0ull};
+  uint32_t p[4] = {NO_INDEX, NO_INDEX, NO_INDEX, NO_INDEX};
+  int id[4] = {-1, -1, -1, -1};
+  for (long long i = (long long)warp * 32 + lane; i < Lc; i += (long long)NW * 32) {
+    const uint64_t kc = skey64(trec[i].s);
+    const uint32_t pc = trec[i].p;
+    const int ic = (int)i;
+    bool b[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) b[j] = (kc > k[j]) | ((kc == k[j]) & (pc < p[j]));
+#pragma unroll
+    for (int j = 3; j >= 1; --j) {  // slot j takes slot j-1 if c beats it, c if c beats only slot j
+      k[j] = b[j] ? (b[j - 1] ? k[j - 1] : kc) : k[j];
+      p[j] = b[j] ? (b[j - 1] ? p[j - 1] : pc) : p[j];
+      id[j] = b[j] ? (b[j - 1] ? id[j - 1] : ic) : id[j];
+    }
+    k[0] = b[0] ? kc : k[0];
+    p[0] = b[0] ? pc : p[0];
+    id[0] = b[0] ? ic : id[0];
+  }
+  // K pops of the lanes' heads (the winner shifts its list)
+  auto pop4 = [&](TkE* out) {
+#pragma unroll
+    for (int t = 0; t < K; ++t) {
+      const uint64_t key = k[0];
+      const uint32_t pp = p[0];
+      const uint32_t hi = (uint32_t)(key >> 32), lo = (uint32_t)key;
+      const uint32_t mhi = __reduce_max_sync(0xffffffffu, hi);
+      unsigned m = __ballot_sync(0xffffffffu, hi == mhi);
+      if (m & (m - 1)) {
+        const uint32_t mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+        m = __ballot_sync(0xffffffffu, hi == mhi && lo == mlo);
+        if (m & (m - 1)) {
+          const bool in = (m >> lane) & 1u;
+          const uint32_t mp = __reduce_min_sync(0xffffffffu, in ? pp : NO_INDEX);
+          m = __ballot_sync(0xffffffffu, in && pp == mp);
+        }
+      }
+      const bool me = lane == __ffs(m) - 1;
+      if (me) {
+        TkE e;
+        e.key = key;
+        e.p = pp;
+        e.id = pp == NO_INDEX ? -1 : id[0];
+        out[t] = e;
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        k[c] = me ? k[c + 1] : k[c];
+        p[c] = me ? p[c + 1] : p[c];
+        id[c] = me ? id[c + 1] : id[c];
+      }
+      k[3] = me ? 0ull : k[3];
+      p[3] = me ? NO_INDEX : p[3];
+      id[3] = me ? -1 : id[3];
+    }
+  };
+  pop4(wk + warp * K);
+  __syncthreads();
+  if (warp == 0) {  // the NW * K warp winners (<= 64: two per lane), sorted per lane, K pops
+    const int n = NW * K;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      k[c] = 0ull;
+      p[c] = NO_INDEX;
+      id[c] = -1;
+    }
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int x = lane + 32 * c;
+      if (x < n) {
+        const TkE e = wk[x];
+        k[c] = e.key;
+        p[c] = e.p;
+        id[c] = e.id;
+      }
+    }
+    const bool sw = (k[1] > k[0]) | ((k[1] == k[0]) & (p[1] < p[0]));
+    if (sw) {
+      const uint64_t tk0 = k[0];
+      const uint32_t tp0 = p[0];
+      const int ti0 = id[0];
+      k[0] = k[1]; p[0] = p[1]; id[0] = id[1];
+      k[1] = tk0; p[1] = tp0; id[1] = ti0;
+    }
+    pop4(wk + 64);
+    __syncwarp();
+    if (lane < K) tk[lane] = wk[64 + lane].id;
+  }
+  __syncthreads();
+}
+
 // global reduced index p -> dictionary u, bin k, frame j (p = off_u + j * M_R,u + k, Z10)
 __device__ __forceinline__ void decode_p(uint32_t p, const DictGeo* sd, int W, int& u, int& k, int& j) {
   u = 0;
@@ -376,7 +486,7 @@ __device__ __forceinline__ unsigned long long gx_ld_acquire(const unsigned long 
 // stamps; the messages are copied into shared memory) and ranking the C*K entries in
 // two stages (the NE best list heads, then their lists' entries); everything else is
 // identical.
-template <typename R, int TW, bool SREC, int K, bool GX>
+template <typename R, int TW, bool SREC, int K, bool GX, bool SCAN = false>
 __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
   using C2 = typename cplx<R>::t;
   using RecT = Rec<R>;
@@ -388,6 +498,8 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
   constexpr int LGTW = TW == 32 ? 5 : (TW == 64 ? 6 : 7);
   constexpr int NCH = TW / 32;
   constexpr int TPI = tiles_per_item<TW>();
+  constexpr bool scan_topk = SCAN;  // top-K by a scan of the tile records (no node tree upkeep)
+  static_assert(!SCAN || (SREC && !GX), "the scan top-K reads shared-memory records of one cluster");
   const int NEc = min(NE, C * K);
   const int B = max(1, min(BMAX, P.spec));
 
@@ -408,6 +520,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
   int* sorted = reinterpret_cast<int*>(smem + L.sorted);
   int* hsel = reinterpret_cast<int*>(smem + L.hsel);
   int* tk = reinterpret_cast<int*>(smem + L.tk);
+  TkE* wk = reinterpret_cast<TkE*>(smem + L.wk);
   int* stamp = reinterpret_cast<int*>(smem + L.stamp);   // dirty-node stamps and lists per level
   int* list = reinterpret_cast<int*>(smem + L.list);
   int* cnt = reinterpret_cast<int*>(smem + L.cnt);
@@ -521,7 +634,8 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
     }
     PROF_MARK(14);
   };
-  cta_topk<R, K>(P, lev, trec, tk, lane, warp, NW);
+  if (scan_topk) cta_topk_scan<R, K>(trec, P.Lc, tk, wk, lane, warp, NW);
+  else cta_topk<R, K>(P, lev, trec, tk, lane, warp, NW);
   if (warp == 0) publish(0, 1ull);
 
   long long rounds = 0;
@@ -1002,7 +1116,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
         trec[l] = rec;
         if constexpr (decltype(upd)::value) atomicMax(&vkey[g], score_key(bs));
         const int node = l >> 5;
-        if (atomicExch(&stamp[node], stampv) != stampv) list[atomicAdd(&cnt[0], 1)] = node;
+        if (!scan_topk && atomicExch(&stamp[node], stampv) != stampv) list[atomicAdd(&cnt[0], 1)] = node;
       }
     };
     // (g, v) of item gi: count the item bases <= gi (ibase is non-decreasing)
@@ -1169,7 +1283,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
     __syncthreads();
     // ---- C. level-0 refresh of the dirty nodes, then the upper levels, one level
     //      at a time, nodes spread over the warps
-    {  // level 0 (children: the tile records)
+    if (!scan_topk) {  // level 0 (children: the tile records)
       const int nl = cnt[0];
       const bool up = P.nlev > 1;
       for (int idx = warp; idx < nl; idx += NW) {
@@ -1187,7 +1301,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
       }
       __syncthreads();
     }
-    for (int l = 1; l < P.nlev; ++l) {
+    for (int l = 1; !scan_topk && l < P.nlev; ++l) {
       const int nl = cnt[l];
       const RecT* child = lev + P.lev_off[l - 1];
       const long long nchild = (long long)P.lev_n[l - 1];
@@ -1213,7 +1327,8 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
       for (int l = 0; l < P.nlev; ++l) cnt[l] = 0;
       if (mode == 1) st->G = 0;  // nothing to verify after a roll-back
     }
-    cta_topk<R, K>(P, lev, trec, tk, lane, warp, NW);
+    if (scan_topk) cta_topk_scan<R, K>(trec, P.Lc, tk, wk, lane, warp, NW);
+    else cta_topk<R, K>(P, lev, trec, tk, lane, warp, NW);
     if (P.prof != nullptr && slot == 0 && tid == 0) {  // per-CTA busy time (receive -> publish) and items
       const unsigned long long busy = (unsigned long long)(clock64() - tbusy0);
       if (rank < 16) atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 40 + rank, busy);
@@ -1235,9 +1350,9 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
   if constexpr (!GX) cg::this_cluster().sync();  // keep shared memory alive until all remote stores are done
 }
 
-template <typename R, int TW, bool SREC, int K, bool GX>
+template <typename R, int TW, bool SREC, int K, bool GX, bool SCAN = false>
 cudaError_t launch_t(const LoopParams& P, int threads, cudaStream_t st) {
-  auto kfn = mp_multi_kernel<R, TW, SREC, K, GX>;
+  auto kfn = mp_multi_kernel<R, TW, SREC, K, GX, SCAN>;
   CUDA_OK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem_bytes));
   if (!GX && P.C > 8) CUDA_OK(cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t cfg = {};
@@ -1306,6 +1421,13 @@ int max_grid_t(int threads, size_t smem) {
 
 template <typename R, bool SREC, bool GX>
 cudaError_t launch_r(const LoopParams& P, int threads, cudaStream_t st) {
+  if constexpr (SREC && !GX) {
+    if (P.topk_scan) switch (P.TW) {
+        case 32: return launch_t<R, 32, true, MULTI_K, false, true>(P, threads, st);
+        case 64: return launch_t<R, 64, true, MULTI_K, false, true>(P, threads, st);
+        case 128: return launch_t<R, 128, true, MULTI_K, false, true>(P, threads, st);
+      }
+  }
   switch (P.TW) {
     case 32: return launch_t<R, 32, SREC, MULTI_K, GX>(P, threads, st);
     case 64: return launch_t<R, 64, SREC, MULTI_K, GX>(P, threads, st);

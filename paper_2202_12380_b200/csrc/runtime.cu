@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -658,6 +659,15 @@ static int ensure_layout(mpgabor* h, int64_t Ls) {
   }
   if (!ok) return h->fail(MPG_ECUDA, "no launch plan for the MP loop: " + why);
   LoopParams& P = h->lp;
+  // multi-selection with shared-memory records on small slices: top-K by a scan of the
+  // tile records instead of the node tree (no tree upkeep per round).  Measured: C1
+  // (~770 records per CTA) 1.24 -> 1.16 us/atom; C2 (~4.4k) 1.79 -> 1.88, so only up to
+  // 2048 records (env MPGABOR_TOPK_SCAN overrides the limit, for measurements)
+  {
+    const char* ev = std::getenv("MPGABOR_TOPK_SCAN");
+    const long long lim = ev ? std::atoll(ev) : 2048;
+    P.topk_scan = (h->kind == 2 && h->srec && !h->gx && P.Lc <= lim) ? 1 : 0;
+  }
   h->lay_C = P.C;
   // buffers
   TRY_CUDA(h, h->d_geo.ensure(sizeof(DictGeo) * W));
