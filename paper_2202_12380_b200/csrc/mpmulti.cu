@@ -730,26 +730,22 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
       const int NL = C * K;
       const int rw = NW == 1 ? 0 : warp - 1, nrw = NW == 1 ? 1 : NW - 1;
       if constexpr (GX) {
-        // stage 1 (C <= 128 heads, 4 lanes per head): the lists whose heads are among
-        // the NEc best heads hold every entry of the window (an entry below the
-        // NEc-th best head has NEc heads ahead of it)
-        for (int grp = rw; grp * 8 < C; grp += nrw) {
-          const int c0 = grp * 8 + (lane >> 2), sub = lane & 3;
-          int cnt = 0;
-          const int ce = c0 < C ? c0 : 0;
-          const uint64_t ke = skey64(mb[ce].list[0].s);
-          const uint32_t pe = mb[ce].list[0].p;
-#pragma unroll 8
-          for (int f = sub; f < 128; f += 4) {  // C <= 128; every load issued before the compares
-            const int fc = f < C ? f : 0;
-            const uint64_t kf = skey64(mb[fc].list[0].s);
-            const uint32_t pf = mb[fc].list[0].p;
-            const bool ahead = (kf > ke) | ((kf == ke) & ((pf < pe) | ((pf == pe) & (f < ce))));
-            cnt += (int)(ahead & (f < C));
+        // stage 1 (one warp, C <= 128 heads, 4 per lane, sorted, NE pops of the lanes'
+        // heads): the lists whose heads are among the NEc best heads hold every entry of
+        // the window (an entry below the NEc-th best head has NEc heads ahead of it)
+        if (rw == 0) {
+          uint64_t hk[4];
+          uint32_t hp4[4];
+          int hi4[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int c = lane + 32 * j;
+            const bool ok = c < C;
+            hk[j] = ok ? skey64(mb[c].list[0].s) : 0ull;
+            hp4[j] = ok ? mb[c].list[0].p : NO_INDEX;
+            hi4[j] = ok ? c : -1;
           }
-          cnt += __shfl_xor_sync(0xffffffffu, cnt, 1);
-          cnt += __shfl_xor_sync(0xffffffffu, cnt, 2);
-          if (c0 < C && sub == 0 && cnt < NEc) hsel[cnt] = c0;
+          warp_topk_nc<NE, 4>(hk, hp4, hi4, hsel, lane);
         }
       }
       for (int grp = rw; !GX && grp * 8 < NL; grp += nrw) {
@@ -791,10 +787,12 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
         static_assert(NE * K <= 32, "stage-2 candidates fit one warp");
         if (warp == 0) {
           const bool have = lane < NEc * K;
-          const int cl = have ? hsel[lane / K] : 0, q = lane % K;
+          const int hs = have ? hsel[lane / K] : -1;
+          const bool hv = hs >= 0;   // (-1: fewer lists than window entries)
+          const int cl = hv ? hs : 0, q = lane % K;
           const int e = cl * K + q;
-          const uint64_t ke = have ? skey64(mb[cl].list[q].s) : 0ull;
-          const uint32_t pe = have ? mb[cl].list[q].p : NO_INDEX;
+          const uint64_t ke = hv ? skey64(mb[cl].list[q].s) : 0ull;
+          const uint32_t pe = hv ? mb[cl].list[q].p : NO_INDEX;
           int cnt = 0;
 #pragma unroll 8
           for (int j = 0; j < 32; ++j) {
@@ -804,7 +802,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
             const bool ahead = (kf > ke) | ((kf == ke) & ((pf < pe) | ((pf == pe) & (ef < e))));
             cnt += (int)((j < NEc * K) & ahead);
           }
-          if (have && cnt < NEc) sorted[cnt] = e;
+          if (hv && cnt < NEc) sorted[cnt] = e;
         }
         __syncthreads();
       }
