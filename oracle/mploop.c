@@ -116,9 +116,18 @@ static void touch(st_t* S, int32_t v, int64_t n) {
   S->touched[S->ntouched++] = S->fr_off[v] + n;
 }
 
-/* second best over all p != pstar (for the near-tie gap report) */
-static double second_best(const st_t* S, int64_t pstar, int64_t fstar) {
+/* second best over all p != pstar (for the near-tie gap report):
+ * s2 = max of the score over every coefficient other than p*.  With the max caches
+ * (up to date before every selection) the frame of p* is rescanned and every other
+ * frame contributes its cached maximum; in full-scan mode the caches are never
+ * refreshed, so s2 is a plain scan over all p != p*. */
+static double second_best(const st_t* S, int64_t pstar, int64_t fstar, int32_t full_scan) {
   double s2 = 0.0;
+  if (full_scan) {
+    for (int64_t p = 0; p < S->P; ++p)
+      if (p != pstar) { double s = score_at(S, p); if (s > s2) s2 = s; }
+    return s2;
+  }
   int32_t w; int64_t n; frame_wn(S, fstar, &w, &n);
   int64_t p0 = S->D[w].off + n * S->D[w].MR;
   for (int64_t p = p0; p < p0 + S->D[w].MR; ++p)
@@ -235,7 +244,7 @@ int orc_mp_run(int32_t W, const orc_dict* D, const orc_kernel* K, double* res, d
     while (u + 1 < W && D[u + 1].off <= ps) ++u;
     int64_t j = (ps - D[u].off) / D[u].MR, k = (ps - D[u].off) % D[u].MR;
     if (gaps) {
-      double s2 = second_best(&S, ps, S.fr_off[u] + j);
+      double s2 = second_best(&S, ps, S.fr_off[u] + j, full_scan);
       gaps[it] = (s1 - s2) / s1;
     }
     /* c. scalar step: c~ (Eq. (19), reading Z11 uses conj(rho)) and E~ (Eq. (20)) */

@@ -105,6 +105,42 @@ def test_maxcache_equals_full_scan():
         assert np.array_equal(r1.energy, r2.energy)
 
 
+def _bruteforce_gap(res):
+    # (s1 - s2)/s1 of the plain score |c^|^2 over every coefficient, s2 over p != argmax
+    s = res.real * res.real + res.imag * res.imag
+    p = int(np.argmax(s))
+    s1 = s[p]
+    s[p] = -1.0
+    return (s1 - s.max()) / s1
+
+
+@pytest.mark.parametrize("full_scan", [False, True])
+def test_gaps_equal_bruteforce_second_best(full_scan):
+    # the near-tie gap gap_k = (s1 - s2)/s1 that decides the fp32
+    # acceptance: at sampled k it equals a brute-force second-best over the residual that
+    # the loop holds before selection k (a run stopped after k selections), in both the
+    # max-cache and the full-scan mode
+    for cfg, ks in ((CONFIGS["C0"], (0, 1, 7, 60, 233, 499)), (CONFIGS["C1"], (0, 5, 111, 640))):
+        x = signal(cfg)
+        S = oracle.Setup.build(x, cfg.dicts, cfg.thr)
+        steps = ks[-1] + 1
+        r = loop.mp_run(S, steps, full_scan=full_scan)
+        assert r.n == steps
+        for k in ks:
+            rk = loop.mp_run(S, k, want_gaps=False)
+            assert r.gaps[k] == _bruteforce_gap(rk.res)
+
+
+def test_gaps_see_an_exact_tie():
+    # two identical separated atoms: the first selection has a gap of exactly 0
+    d = Dict(HANN, 16, 4, 16)
+    L = 128
+    x = 2 * np.real(dense.atom(d, 3, 4, L)) + 2 * np.real(dense.atom(d, 3, 20, L))
+    S = oracle.Setup.build(x, (d,), 1e-4)
+    for fs in (False, True):
+        assert loop.mp_run(S, 2, full_scan=fs).gaps[0] == 0.0
+
+
 def test_tie_break_lowest_index():
     # Z10: exact ties go to the lowest global index.  Two identical well separated
     # pair atoms in the same dictionary -> the earlier frame is selected first.
