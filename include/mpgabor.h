@@ -111,11 +111,15 @@ int mpgabor_kernels(mpgabor* h, double thr, void* cuda_stream);
 
 /* Geometry for a signal of Ls samples (host outputs, each may be NULL):
  * L_pad, and per dictionary w: N[w] frames, M_R[w] = M_w/2+1 reduced bins,
+ * row_stride[w] = elements between consecutive frames of dictionary w in every
+ * coefficient vector this API exchanges (coef_dev of mpgabor_run, the export of
+ * mpgabor_residual) -- these are dense, so row_stride[w] = M_R[w]; the library's
+ * internal residual grids pad rows to whole tiles and stay private --
  * coef_offset[w] = global index of (w, n=0, m=0) in the coefficient vector
- * (index p = coef_offset[w] + n*M_R[w] + m, Z10), coef_offset[W] =
- * total number of reduced coefficients P_R.  Pure host computation. */
+ * (index p = coef_offset[w] + n*row_stride[w] + m, Z10), coef_offset[W] =
+ * total number of reduced coefficients P_R.  Pure host computation (SURVEY §8(b)). */
 int mpgabor_layout(const mpgabor* h, int64_t Ls, int64_t* L_pad, int64_t* N, int64_t* M_R,
-                   int64_t* coef_offset);
+                   int64_t* row_stride, int64_t* coef_offset);
 
 /* Run coefficient-domain MP (Alg. 1 P:356-387 with Eq. (9) P:424-434 and Alg. 3
  * P:978-1029) on x_dev (device fp64[Ls]):

@@ -42,7 +42,9 @@ struct LoopResult {
   int pad;
   double E_final;
   long long rounds;              // loop rounds (multi-selection kernel; = n_done + 1 for the others)
+  double E0;                     // E_0 = ||x||^2 of the slot (copied from E0v by the loop kernel)
 };
+constexpr int STOP_NONFINITE = -1;  // LoopResult.stop: x held NaN/Inf, the loop did not run
 
 constexpr int MAX_LEVELS = 6;
 constexpr int MPG_PROF_SLOTS = 320;  // mpgabor_last_profile slots
@@ -70,7 +72,7 @@ struct LoopParams {
   const void* kern;              // kernels (cplx<R>), per-class layout
   void* rec;                     // Rec<R>[C * Lc] (initial records; the live ones when !srec)
   long long maxit;
-  double Etol, E0;
+  double E0;
   AtomOut* atoms;
   double* energy;
   double2* sol;                  // may be null
@@ -81,8 +83,10 @@ struct LoopParams {
   void* gx_rec;                  // grid mode: one-selection kernel Rec<R>[2][C] roots, multi-selection
                                  //   kernel its [2][C] messages, in global memory (else null)
   unsigned long long* gx_stamp;  // [2][C] round stamps of gx_rec (zeroed before the launch)
-  const double* E0v;             // batched signals (one-selection cluster kernel): per-slot E_0, stop level
-  const double* Etolv;           //   (null: the scalars E0 / Etol)
+  const double* E0v;             // per-slot E_0 (device, written by the energy kernel; null: the scalar E0)
+  const int* nonfinite;          // device flag set by the energy kernel when x holds NaN/Inf (null: none)
+  int etol_mode;                 // stop level per slot: 0 none (-inf), 1 etol_val * E0v[slot], 2 etol_val
+  double etol_val;               //   (10^(errdb/10) for mode 1; an absolute level for mode 2)
   long long slot_grid;           //   grid elements per slot; the records per slot are C * Lc
   long long slot_atoms;          //   atoms per slot (= maxit); energies per slot = slot_atoms + 1
   int nslot;                     //   signals (clusters) of the launch
@@ -115,8 +119,9 @@ size_t multi_msg_bytes(bool f64);
 
 
 // synthesis (synth.cu)
+// first: uint32[P_R] all 0xff, done: uint8[n_atoms] all 0, ctl: uint32[3] all 0 (scratch)
 cudaError_t launch_synth_scatter(const AtomOut* atoms, int64_t n_atoms, const DictGeo* dg_dev, int W, double2* sol,
-                                 cudaStream_t st);
+                                 unsigned int* first, unsigned char* done, unsigned int* ctl, cudaStream_t st);
 cudaError_t launch_synth_frames(const double2* sol, const DictGeo& d, const double2* tw, int twres, double* frames,
                                 cudaStream_t st);
 cudaError_t launch_sub(double* r, const double* y, int64_t n, cudaStream_t st);  // r -= y

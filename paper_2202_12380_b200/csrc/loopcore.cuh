@@ -237,9 +237,18 @@ __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
 __device__ __forceinline__ void mbar_arm(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
+// Inter-CTA waits are bounded: a peer that never arrives (a logic error, or a CTA that
+// left the loop early) traps after ~2^35 SM cycles (~17 s) instead of hanging the GPU;
+// the launch then fails with a CUDA error (MPG_ECUDA) instead of spinning forever.
+constexpr long long SPIN_LIMIT_CYCLES = 1LL << 35;
+__device__ __forceinline__ void spin_check(long long t0) {
+  if (clock64() - t0 > SPIN_LIMIT_CYCLES) __trap();
+}
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   uint32_t ok = 0;
+  const long long t0 = clock64();
   do {
+    spin_check(t0);
     asm volatile(
         "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
         : "=r"(ok)

@@ -137,7 +137,17 @@ __global__ void __launch_bounds__(512, 1) mp_loop_kernel(const LoopParams P) {
   // records, atoms, energies and result; the kernels are shared)
   const int slot = GX ? 0 : (int)(blockIdx.x / (unsigned)C);
   const double E0s = P.E0v ? P.E0v[slot] : P.E0;
-  const double Etols = P.Etolv ? P.Etolv[slot] : P.Etol;
+  const double Etols = P.etol_mode == 1 ? P.etol_val * E0s : (P.etol_mode == 2 ? P.etol_val : -INFINITY);
+  if (P.nonfinite != nullptr && *P.nonfinite) {  // x holds NaN/Inf: report, run nothing (uniform exit)
+    if (rank == 0 && threadIdx.x == 0) {
+      P.result[slot].n_done = 0;
+      P.result[slot].stop = STOP_NONFINITE;
+      P.result[slot].E_final = E0s;
+      P.result[slot].rounds = 0;
+      P.result[slot].E0 = E0s;
+    }
+    return;
+  }
   AtomOut* atoms_out = P.atoms + (long long)slot * P.slot_atoms;
   double* energy_out = P.energy + (long long)slot * (P.slot_atoms + 1);
   RecT* grec = reinterpret_cast<RecT*>(P.rec) + (long long)slot * C * P.Lc + (long long)rank * P.Lc;
@@ -225,9 +235,12 @@ __global__ void __launch_bounds__(512, 1) mp_loop_kernel(const LoopParams P) {
     if (!GX && warp < 2) mbar_wait(smem_addr(&mbar[par]), (uint32_t)((it >> 1) & 1));
     if (GX && warp < 2) {  // every CTA's root of this iteration: stamps == it + 1
       const unsigned long long want = (unsigned long long)it + 1;
-      for (int c = lane; c < C; c += 32)
+      for (int c = lane; c < C; c += 32) {
+        const long long t0 = clock64();
         while (ld_acquire_u64(P.gx_stamp + par * C + c) != want) {
+          spin_check(t0);
         }
+      }
       __syncwarp();
     }
     PROF_MARK(0);
@@ -493,6 +506,7 @@ __global__ void __launch_bounds__(512, 1) mp_loop_kernel(const LoopParams P) {
     P.result[slot].n_done = it;
     P.result[slot].stop = stop;
     P.result[slot].E_final = sel->E[it & 1];
+    P.result[slot].E0 = E0s;
   }
   if (prof) {
     for (int i = 0; i < 7; ++i) P.prof[i] = ph[i];

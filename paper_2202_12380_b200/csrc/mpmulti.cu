@@ -114,7 +114,27 @@ struct TkE {              // a top-K candidate: order key, index, id (tile; -1 =
 
 struct Smem {
   size_t mbar, mail, mymsg, trec, lev, ent, egeo, wmask, rect, ecnt, st, vkey, sorted, hsel, tk, wk, stamp, list, cnt, pairs, dicts, own, roots,
-      rho, rho_meta, total;
+      rho, rho_meta, cls, clid, hist, inl, total;
+};
+
+// Candidate list of a CTA (top-K mode 2): the tiles whose score key is >= theta, held
+// across rounds.  Invariant: every tile NOT in the list has key < theta, so the K best
+// list entries are the CTA's exact top K whenever at least K entries remain (or theta
+// is the smallest positive key: the CTA has fewer than K positive tiles, and empty
+// records stand for its zero tiles).  A round only adds the tiles its items rewrote and
+// that reach theta, and drops entries that fell below it; when fewer than K remain (or
+// the list overflows) it is rebuilt by a radix select of theta over all tile records.
+constexpr int CL_CAP = 128;      // list capacity (4 entries per lane of one warp)
+constexpr int CL_TARGET = 48;    // entries a rebuild aims at
+struct ClState {
+  uint64_t theta;                // list threshold (order key of the score, >= 1)
+  uint64_t prefix;               // radix select: key prefix of the current range
+  int n;                         // entries (may exceed CL_CAP: overflow -> rebuild)
+  int above;                     // radix select: entries above the current range
+  int done;                      // radix select finished
+  int valid;                     // 0: the rebuild could not make an exact list (ties) -> scan
+  int need;                      // 1: rebuild before the next extraction
+  int pad_;
 };
 
 __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -187,6 +207,15 @@ __host__ __device__ inline Smem smem_layout(const LoopParams& P, size_t recsz, s
   o += sizeof(RhoEnt) * P.rho_total;
   s.rho_meta = o;
   o += sizeof(int) * 3 * P.W;
+  o = align_up(o, 16);
+  s.cls = o;
+  o += P.topk_scan == 2 ? sizeof(ClState) : 0;
+  s.clid = o;
+  o += P.topk_scan == 2 ? sizeof(int) * CL_CAP : 0;
+  s.hist = o;
+  o += P.topk_scan == 2 ? sizeof(int) * 256 : 0;
+  s.inl = o;
+  o += P.topk_scan == 2 ? (size_t)P.Lc : 0;
   s.total = align_up(o, 16);
   return s;
 }
@@ -438,6 +467,157 @@ __device__ __forceinline__ void cta_topk_scan(const Rec<R>* trec, long long Lc, 
   __syncthreads();
 }
 
+// Candidate-list rebuild (all threads; needs a barrier before, ends with one): theta =
+// the lower bound of the 8-bit radix bucket (of the 64-bit score key, most significant
+// byte first, positive keys only) in which the count of keys from the top reaches
+// CL_TARGET, refined byte by byte until the count is <= CL_CAP; then the list = every
+// tile with key >= theta.  Exact ties wider than CL_CAP at the last byte leave theta just
+// above the tied key; if fewer than K tiles remain above it, the list is marked invalid
+// (the caller extracts by a full scan until a later rebuild succeeds).
+template <typename R, int K>
+__device__ __noinline__ void cl_rebuild(const Rec<R>* trec, long long Lc, ClState* cs, int* clid, int* hist,
+                                        unsigned char* inl, int lane, int warp) {
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  for (long long i = tid; i < Lc; i += nthr) inl[i] = 0;
+  if (tid == 0) {
+    cs->prefix = 0;
+    cs->above = 0;
+    cs->done = 0;
+    cs->n = 0;
+    cs->valid = 1;
+  }
+  for (int pass = 0; pass < 8; ++pass) {
+    const int shift = 56 - 8 * pass;
+    for (int i = tid; i < 256; i += nthr) hist[i] = 0;
+    __syncthreads();
+    const uint64_t pre = cs->prefix;
+    for (long long i = tid; i < Lc; i += nthr) {
+      const uint64_t key = skey64(trec[i].s);
+      const bool inr = key != 0ull && (pass == 0 || (key >> (shift + 8)) == pre);
+      if (inr) atomicAdd(&hist[(int)((key >> shift) & 255ull)], 1);
+    }
+    __syncthreads();
+    if (warp == 0) {
+      // lane l holds bins 255 - 8l - j (j < 8), i.e. the bins in descending order
+      int c[8], sum = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        c[j] = hist[255 - 8 * lane - j];
+        sum += c[j];
+      }
+      int incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int above = cs->above;
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      const uint64_t lo_bound = pass == 0 ? 1ull : (pre << (shift + 8));  // lowest key of the range
+      if (above + total < CL_TARGET) {  // every positive key of the range fits
+        if (lane == 0) {
+          cs->theta = lo_bound;
+          cs->done = 1;
+        }
+      } else {
+        // the first bin (descending) whose cumulative count reaches the target
+        const int excl = incl - sum;
+        int run = excl, hitj = -1;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int before = run;
+          run += c[j];
+          if (hitj < 0 && above + before < CL_TARGET && above + run >= CL_TARGET) hitj = j;
+        }
+        const unsigned hm = __ballot_sync(0xffffffffu, hitj >= 0);
+        const int hl = __ffs(hm) - 1;
+        if (lane == hl) {
+          const int b = 255 - 8 * lane - hitj;
+          int cum_above = excl;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) cum_above += j < hitj ? c[j] : 0;
+          const int cnt = above + cum_above + c[hitj];
+          const uint64_t bkey = ((pre << 8) | (uint64_t)b) << shift;
+          if (cnt <= CL_CAP) {
+            cs->theta = bkey > 0ull ? bkey : 1ull;
+            cs->done = 1;
+          } else if (pass == 7) {  // one key value tied wider than the capacity
+            cs->theta = bkey + 1ull;
+            cs->valid = above + cum_above >= K ? 1 : 0;
+            cs->done = 1;
+          } else {
+            cs->above = above + cum_above;
+            cs->prefix = (pre << 8) | (uint64_t)b;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (cs->done) break;
+  }
+  const uint64_t th = cs->theta;
+  for (long long i = tid; i < Lc; i += nthr) {
+    if (skey64(trec[i].s) >= th) {
+      inl[i] = 1;
+      const int idx = atomicAdd(&cs->n, 1);
+      if (idx < CL_CAP) clid[idx] = (int)i;
+    }
+  }
+  __syncthreads();
+}
+
+// Candidate-list extraction (warp 0): drop the entries that fell below theta (clearing
+// their membership flags), compact the list, and pop the K best (score key desc, index
+// asc) into tk[0..K-1] (-1 = none).  Returns (to every lane) whether the result is the
+// CTA's exact top K (see ClState); if not, the caller rebuilds and extracts again.
+template <typename R, int K>
+__device__ __forceinline__ bool cl_extract(const Rec<R>* trec, ClState* cs, int* clid, unsigned char* inl, int* tk,
+                                           int lane) {
+  static_assert(CL_CAP == 128 && K == 4, "4 list entries per lane, sorted 4-lists");
+  const int n = cs->n;
+  const uint64_t th = cs->theta;
+  uint64_t kk[4];
+  uint32_t pk[4];
+  int ik[4];
+  int base = 0;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {  // read every slot first (the compaction below overwrites them)
+    const int slot = c * 32 + lane;
+    const int id = slot < n && slot < CL_CAP ? clid[slot] : -1;
+    uint64_t key = 0ull;
+    uint32_t p = NO_INDEX;
+    if (id >= 0) {
+      key = skey64(trec[id].s);
+      p = trec[id].p;
+    }
+    const bool keep = id >= 0 && key >= th;
+    if (id >= 0 && !keep) inl[id] = 0;
+    base += __popc(__ballot_sync(0xffffffffu, keep));
+    kk[c] = keep ? key : 0ull;
+    pk[c] = keep ? p : NO_INDEX;
+    ik[c] = keep ? id : -1;
+  }
+  __syncwarp();
+  // write the compacted list after every slot has been read
+  {
+    int b2 = 0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const bool keep = ik[c] >= 0;
+      const unsigned km = __ballot_sync(0xffffffffu, keep);
+      const int pos = b2 + __popc(km & ((1u << lane) - 1u));
+      b2 += __popc(km);
+      if (keep) clid[pos] = ik[c];
+    }
+  }
+  __syncwarp();
+  const bool overflow = n > CL_CAP;
+  if (lane == 0) cs->n = base;
+  warp_topk_nc<K, 4>(kk, pk, ik, tk, lane);
+  __syncwarp();
+  return !overflow && (base >= K || th == 1ull);
+}
+
 // global reduced index p -> dictionary u, bin k, frame j (p = off_u + j * M_R,u + k, Z10)
 __device__ __forceinline__ void decode_p(uint32_t p, const DictGeo* sd, int W, int& u, int& k, int& j) {
   u = 0;
@@ -486,7 +666,9 @@ __device__ __forceinline__ unsigned long long gx_ld_acquire(const unsigned long 
 // stamps; the messages are copied into shared memory) and ranking the C*K entries in
 // two stages (the NE best list heads, then their lists' entries); everything else is
 // identical.
-template <typename R, int TW, bool SREC, int K, bool GX, bool SCAN = false>
+// TOPK: how a CTA finds its K best tiles each round -- 0 down the 32-ary node tree, 1 by a
+// scan of all its tile records, 2 from its candidate list (ClState).
+template <typename R, int TW, bool SREC, int K, bool GX, int TOPK = 0>
 __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
   using C2 = typename cplx<R>::t;
   using RecT = Rec<R>;
@@ -498,8 +680,8 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
   constexpr int LGTW = TW == 32 ? 5 : (TW == 64 ? 6 : 7);
   constexpr int NCH = TW / 32;
   constexpr int TPI = tiles_per_item<TW>();
-  constexpr bool scan_topk = SCAN;  // top-K by a scan of the tile records (no node tree upkeep)
-  static_assert(!SCAN || (SREC && !GX), "the scan top-K reads shared-memory records of one cluster");
+  constexpr bool notree = TOPK != 0;  // top-K without the node tree (no tree upkeep per round)
+  static_assert(TOPK == 0 || SREC, "the scan / list top-K read shared-memory tile records");
   const int NEc = min(NE, C * K);
   const int B = max(1, min(BMAX, P.spec));
 
@@ -532,11 +714,25 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
   int* rho_lo = reinterpret_cast<int*>(smem + L.rho_meta);
   int* rho_n = rho_lo + W;
   int* rho_off = rho_n + W;
+  ClState* cls = reinterpret_cast<ClState*>(smem + L.cls);
+  int* clid = reinterpret_cast<int*>(smem + L.clid);
+  int* hist = reinterpret_cast<int*>(smem + L.hist);
+  unsigned char* inl = smem + L.inl;
   // batched independent signals: cluster `slot` works on signal `slot` (its own grids,
   // records, backups, atoms, energies, result; the kernels are shared)
   const int slot = GX ? 0 : (int)(blockIdx.x / (unsigned)C);
   const double E0s = P.E0v ? P.E0v[slot] : P.E0;
-  const double Etols = P.Etolv ? P.Etolv[slot] : P.Etol;
+  const double Etols = P.etol_mode == 1 ? P.etol_val * E0s : (P.etol_mode == 2 ? P.etol_val : -INFINITY);
+  if (P.nonfinite != nullptr && *P.nonfinite) {  // x holds NaN/Inf: report, run nothing (uniform exit)
+    if (rank == 0 && threadIdx.x == 0) {
+      P.result[slot].n_done = 0;
+      P.result[slot].stop = STOP_NONFINITE;
+      P.result[slot].E_final = E0s;
+      P.result[slot].rounds = 0;
+      P.result[slot].E0 = E0s;
+    }
+    return;
+  }
   AtomOut* atoms_out = P.atoms + (long long)slot * P.slot_atoms;
   double* energy_out = P.energy + (long long)slot * (P.slot_atoms + 1);
   RecT* grec = reinterpret_cast<RecT*>(P.rec) + (long long)slot * C * P.Lc + (long long)rank * P.Lc;
@@ -634,8 +830,39 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
     }
     PROF_MARK(14);
   };
-  if (scan_topk) cta_topk_scan<R, K>(trec, P.Lc, tk, wk, lane, warp, NW);
-  else cta_topk<R, K>(P, lev, trec, tk, lane, warp, NW);
+  // this CTA's K best tiles into tk[0..K-1] (all threads; a barrier before, ends with one)
+  auto topk = [&]() {
+    if constexpr (TOPK == 2) {
+      if (warp == 0) {
+        const bool ok = cls->valid && !cls->need && cl_extract<R, K>(trec, cls, clid, inl, tk, lane);
+        if (lane == 0) cls->need = ok ? 0 : 1;
+      }
+      __syncthreads();
+      if (cls->need) {  // rebuild the list, extract again; a full scan if it cannot be exact
+        if (prof) atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 19, 1ull);
+        cl_rebuild<R, K>(trec, P.Lc, cls, clid, hist, inl, lane, warp);
+        if (warp == 0) {
+          const bool ok = cls->valid && cl_extract<R, K>(trec, cls, clid, inl, tk, lane);
+          if (lane == 0) cls->need = ok ? 0 : 1;
+        }
+        __syncthreads();
+        if (cls->need) cta_topk_scan<R, K>(trec, P.Lc, tk, wk, lane, warp, NW);
+      }
+    } else if constexpr (TOPK == 1) {
+      cta_topk_scan<R, K>(trec, P.Lc, tk, wk, lane, warp, NW);
+    } else {
+      cta_topk<R, K>(P, lev, trec, tk, lane, warp, NW);
+    }
+  };
+  if constexpr (TOPK == 2) {
+    if (tid == 0) {
+      cls->need = 1;
+      cls->valid = 1;
+      cls->n = 0;
+    }
+    __syncthreads();
+  }
+  topk();
   if (warp == 0) publish(0, 1ull);
 
   long long rounds = 0;
@@ -649,7 +876,9 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
       const unsigned long long want = (unsigned long long)round + 1;
       constexpr int NCHUNK = (int)(sizeof(MsgT) / 16);
       for (int c = tid; c < C; c += blockDim.x) {
+        const long long t0 = clock64();
         while (gx_ld_acquire(P.gx_stamp + (long long)par * C + c) != want) {
+          spin_check(t0);
         }
         const uint4* srcg = reinterpret_cast<const uint4*>(reinterpret_cast<const MsgT*>(P.gx_rec) + (long long)par * C + c);
         uint4* dsts = reinterpret_cast<uint4*>(mail + c);
@@ -741,8 +970,12 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
           for (int j = 0; j < 4; ++j) {
             const int c = lane + 32 * j;
             const bool ok = c < C;
+            // an empty list (a CTA owning no frames) keeps its id: its head takes the index
+            // NO_INDEX - 1 (no real p reaches it), so the NEc pops always name real lists and
+            // stage 2 fills every window slot (lists past C stay NO_INDEX, id -1)
+            const uint32_t hpc = ok ? mb[c].list[0].p : NO_INDEX;
             hk[j] = ok ? skey64(mb[c].list[0].s) : 0ull;
-            hp4[j] = ok ? mb[c].list[0].p : NO_INDEX;
+            hp4[j] = ok && hpc == NO_INDEX ? NO_INDEX - 1u : hpc;
             hi4[j] = ok ? c : -1;
           }
           warp_topk_nc<NE, 4>(hk, hp4, hi4, hsel, lane);
@@ -788,7 +1021,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
         if (warp == 0) {
           const bool have = lane < NEc * K;
           const int hs = have ? hsel[lane / K] : -1;
-          const bool hv = hs >= 0;   // (-1: fewer lists than window entries)
+          const bool hv = hs >= 0;   // (always: C >= 32 > NE lists, empty ones included)
           const int cl = hv ? hs : 0, q = lane % K;
           const int e = cl * K + q;
           const uint64_t ke = hv ? skey64(mb[cl].list[q].s) : 0ull;
@@ -1103,6 +1336,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
     // ---- B. residual update (or roll-back) over this CTA's rows ------------
     // tile bookkeeping: record, candidate maximum, dirty level-0 node (stamp + list)
     const int stampv = round + 1;
+    const uint64_t theta = TOPK == 2 ? cls->theta : 0ull;
     auto finish = [&](int l, int g, R bs, uint32_t bp, R bre, R bim, auto upd) {
       if (lane == warp_argmax_lane(bs, bp)) {
         RecT rec;
@@ -1113,8 +1347,15 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
         if constexpr (sizeof(R) == 8) rec.pad = 0;
         trec[l] = rec;
         if constexpr (decltype(upd)::value) atomicMax(&vkey[g], score_key(bs));
+        if constexpr (TOPK == 2) {  // a rewritten tile at or above theta joins the candidate list
+          if (skey64(bs) >= theta && !inl[l]) {
+            inl[l] = 1;
+            const int idx = atomicAdd(&cls->n, 1);
+            if (idx < CL_CAP) clid[idx] = (int)l;
+          }
+        }
         const int node = l >> 5;
-        if (!scan_topk && atomicExch(&stamp[node], stampv) != stampv) list[atomicAdd(&cnt[0], 1)] = node;
+        if (!notree && atomicExch(&stamp[node], stampv) != stampv) list[atomicAdd(&cnt[0], 1)] = node;
       }
     };
     // (g, v) of item gi: count the item bases <= gi (ibase is non-decreasing)
@@ -1281,7 +1522,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
     __syncthreads();
     // ---- C. level-0 refresh of the dirty nodes, then the upper levels, one level
     //      at a time, nodes spread over the warps
-    if (!scan_topk) {  // level 0 (children: the tile records)
+    if (!notree) {  // level 0 (children: the tile records)
       const int nl = cnt[0];
       const bool up = P.nlev > 1;
       for (int idx = warp; idx < nl; idx += NW) {
@@ -1299,7 +1540,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
       }
       __syncthreads();
     }
-    for (int l = 1; !scan_topk && l < P.nlev; ++l) {
+    for (int l = 1; !notree && l < P.nlev; ++l) {
       const int nl = cnt[l];
       const RecT* child = lev + P.lev_off[l - 1];
       const long long nchild = (long long)P.lev_n[l - 1];
@@ -1325,8 +1566,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
       for (int l = 0; l < P.nlev; ++l) cnt[l] = 0;
       if (mode == 1) st->G = 0;  // nothing to verify after a roll-back
     }
-    if (scan_topk) cta_topk_scan<R, K>(trec, P.Lc, tk, wk, lane, warp, NW);
-    else cta_topk<R, K>(P, lev, trec, tk, lane, warp, NW);
+    topk();
     if (P.prof != nullptr && slot == 0 && tid == 0) {  // per-CTA busy time (receive -> publish) and items
       const unsigned long long busy = (unsigned long long)(clock64() - tbusy0);
       if (rank < 16) atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 40 + rank, busy);
@@ -1342,15 +1582,16 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
     P.result[slot].stop = st->stop;
     P.result[slot].E_final = st->E;
     P.result[slot].rounds = rounds;
+    P.result[slot].E0 = E0s;
   }
   if (prof) P.prof[15] = rounds;
 #undef PROF_MARK
   if constexpr (!GX) cg::this_cluster().sync();  // keep shared memory alive until all remote stores are done
 }
 
-template <typename R, int TW, bool SREC, int K, bool GX, bool SCAN = false>
+template <typename R, int TW, bool SREC, int K, bool GX, int TOPK = 0>
 cudaError_t launch_t(const LoopParams& P, int threads, cudaStream_t st) {
-  auto kfn = mp_multi_kernel<R, TW, SREC, K, GX, SCAN>;
+  auto kfn = mp_multi_kernel<R, TW, SREC, K, GX, TOPK>;
   CUDA_OK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem_bytes));
   if (!GX && P.C > 8) CUDA_OK(cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t cfg = {};
@@ -1420,10 +1661,15 @@ int max_grid_t(int threads, size_t smem) {
 template <typename R, bool SREC, bool GX>
 cudaError_t launch_r(const LoopParams& P, int threads, cudaStream_t st) {
   if constexpr (SREC && !GX) {
-    if (P.topk_scan) switch (P.TW) {
-        case 32: return launch_t<R, 32, true, MULTI_K, false, true>(P, threads, st);
-        case 64: return launch_t<R, 64, true, MULTI_K, false, true>(P, threads, st);
-        case 128: return launch_t<R, 128, true, MULTI_K, false, true>(P, threads, st);
+    if (P.topk_scan == 1) switch (P.TW) {
+        case 32: return launch_t<R, 32, true, MULTI_K, false, 1>(P, threads, st);
+        case 64: return launch_t<R, 64, true, MULTI_K, false, 1>(P, threads, st);
+        case 128: return launch_t<R, 128, true, MULTI_K, false, 1>(P, threads, st);
+      }
+    if (P.topk_scan == 2) switch (P.TW) {
+        case 32: return launch_t<R, 32, true, MULTI_K, false, 2>(P, threads, st);
+        case 64: return launch_t<R, 64, true, MULTI_K, false, 2>(P, threads, st);
+        case 128: return launch_t<R, 128, true, MULTI_K, false, 2>(P, threads, st);
       }
   }
   switch (P.TW) {

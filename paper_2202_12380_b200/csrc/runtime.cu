@@ -81,7 +81,7 @@ struct mpgabor {
   bool batch_mode = false;    // batched signals: one cluster per signal
   int batch_C = 16;           // batched signals: automatic cluster size per signal
   int pedantic = 0;           // 1: pedantic selection (Eq. (20) energies)
-  DevBuf etolv;               // batched signals: per-signal stop levels
+  DevBuf sfirst, sdone;       // synthesis scratch: first atom per coefficient, retired atoms + control words
   DevBuf gxrec, gxstamp;
 
   // per-length layout
@@ -204,7 +204,7 @@ extern "C" void mpgabor_destroy(mpgabor* h) {
     cudaSetDevice(h->device);
     for (DevBuf* b : {&h->tw, &h->roots, &h->win, &h->kern, &h->boxcopy, &h->d_pairs, &h->rho, &h->rho_meta,
                       &h->Hscratch, &h->mxbox, &h->d_geo, &h->grid, &h->rec, &h->xp, &h->partial, &h->flag,
-                      &h->E0, &h->result, &h->sol, &h->frames, &h->hx, &h->hatoms, &h->henergy, &h->hy, &h->prof, &h->d_own, &h->backup, &h->gxrec, &h->gxstamp, &h->rr, &h->yy, &h->etolv})
+                      &h->E0, &h->result, &h->sol, &h->frames, &h->hx, &h->hatoms, &h->henergy, &h->hy, &h->prof, &h->d_own, &h->backup, &h->gxrec, &h->gxstamp, &h->rr, &h->yy, &h->sfirst, &h->sdone})
       b->release();
     for (auto e : h->ev)
       if (e) cudaEventDestroy(e);
@@ -414,7 +414,7 @@ static int64_t ell_of(const mpgabor* h) {
 }
 
 extern "C" int mpgabor_layout(const mpgabor* h, int64_t Ls, int64_t* L_pad, int64_t* N, int64_t* M_R,
-                              int64_t* coef_offset) {
+                              int64_t* row_stride, int64_t* coef_offset) {
   if (!h) return MPG_EINVAL;
   if (Ls < 1) return const_cast<mpgabor*>(h)->fail(MPG_EINVAL, "Ls must be >= 1");
   const int64_t ell = ell_of(h);
@@ -426,6 +426,7 @@ extern "C" int mpgabor_layout(const mpgabor* h, int64_t Ls, int64_t* L_pad, int6
     const int64_t n = L / h->dicts[w].a, mr = h->dicts[w].M / 2 + 1;
     if (N) N[w] = n;
     if (M_R) M_R[w] = mr;
+    if (row_stride) row_stride[w] = mr;  // exchanged coefficient vectors are dense
     if (coef_offset) coef_offset[w] = off;
     off += n * mr;
   }
@@ -485,14 +486,14 @@ static int plan_grids(mpgabor* h, int64_t L, int TW) {
 }
 
 // Automatic choice between the loop kernels (mpgabor_set_batch 0).  A multi-selection
-// round has a fixed cost of ~12k SM cycles (list exchange, ranking, walk, top-K) and
-// yields ~5 atoms; an iteration of the one-selection loop costs ~5k cycles plus its
-// share of the update.  Measured on B200: multi-selection wins while
-// an atom's update is moderate (C1: 643 coefficients, 1.42 vs 2.52 us/atom; C2: 2,086,
-// 2.05 vs 2.72; C3: 18.6k) and loses on C4 (54k, where the one-selection loop runs on a
-// 64-CTA grid).  Estimate the mean update size from the kernel boxes (subsampled per
-// target, averaged over the selected dictionary) and require it to be a small fraction
-// of the grid.
+// round has a fixed cost (list exchange, ranking, walk, candidate lists) and yields
+// several atoms; an iteration of the one-selection loop pays the exchange for every atom.
+// Measured on B200 (profiles/r01_configs.md, full runs, us/atom one-selection vs multi):
+// C0 2.25 vs 2.03, C1 2.52 vs 1.16, C2 2.72 vs 1.79, C3 5.42 vs 2.54 (grid 64), C4 9.63
+// vs 5.61 (grid 128): multi-selection wins on every config.  It needs atoms whose
+// updates are mostly disjoint, so it is taken while the mean update (kernel boxes,
+// subsampled per target, averaged over the selected dictionary) is a small fraction of
+// the grid (C0: 2.6 %).
 static double mean_update(const mpgabor* h) {
   const int W = h->W;
   double sum = 0.0;
@@ -506,10 +507,8 @@ static double mean_update(const mpgabor* h) {
 
 static bool auto_multi(const mpgabor* h, int64_t P_R) {
   const double per_atom = mean_update(h);
-  // rounds need independent atoms: small patches relative to the grid (C0's patch
-  // covers 2.6 % of its grid and gives ~2 atoms per round)
   // (wide updates run the multi-selection kernel as a grid of 64 / 128 CTAs, below)
-  return per_atom < 0.005 * (double)P_R;
+  return per_atom < 0.05 * (double)P_R;
 }
 static bool auto_multi(const mpgabor* h) { return auto_multi(h, h->P_R); }
 
@@ -659,14 +658,21 @@ static int ensure_layout(mpgabor* h, int64_t Ls) {
   }
   if (!ok) return h->fail(MPG_ECUDA, "no launch plan for the MP loop: " + why);
   LoopParams& P = h->lp;
-  // multi-selection with shared-memory records on small slices: top-K by a scan of the
-  // tile records instead of the node tree (no tree upkeep per round).  Measured: C1
-  // (~770 records per CTA) 1.24 -> 1.16 us/atom; C2 (~4.4k) 1.79 -> 1.88, so only up to
-  // 2048 records (env MPGABOR_TOPK_SCAN overrides the limit, for measurements)
+  // multi-selection with shared-memory records: each CTA's top K from its candidate list
+  // (mpmulti.cu ClState: tiles at or above a threshold, kept across rounds, rebuilt by a
+  // radix select when it runs short) instead of the node tree (2) or a scan of every
+  // record (1); env MPGABOR_TOPK = 0/1/2 overrides, for measurements
   {
-    const char* ev = std::getenv("MPGABOR_TOPK_SCAN");
-    const long long lim = ev ? std::atoll(ev) : 2048;
-    P.topk_scan = (h->kind == 2 && h->srec && !h->gx && P.Lc <= lim) ? 1 : 0;
+    const char* ev = std::getenv("MPGABOR_TOPK");
+    const int want = ev ? std::atoi(ev) : 2;
+    P.topk_scan = (h->kind == 2 && h->srec && !h->gx) ? std::max(0, std::min(2, want)) : 0;
+    if (P.topk_scan) {  // the list's shared memory (membership flags per record) must fit
+      P.smem_bytes = multi_smem_bytes(P, h->f64());
+      if (P.smem_bytes > 227 * 1024) {
+        P.topk_scan = 0;
+        P.smem_bytes = multi_smem_bytes(P, h->f64());
+      }
+    }
   }
   h->lay_C = P.C;
   // buffers
@@ -771,7 +777,6 @@ static int run_impl(mpgabor* h, const double* x_dev, int64_t Ls, int64_t maxit, 
   }
   TRY_CUDA(h, h->E0.ensure(sizeof(double) * B));
   TRY_CUDA(h, h->result.ensure(sizeof(LoopResult) * B));
-  TRY_CUDA(h, h->etolv.ensure(sizeof(double) * B));
   const size_t recsz = h->f64() ? sizeof(Rec<double>) : sizeof(Rec<float>);
   TRY_CUDA(h, cudaEventRecord(h->ev[0], st));
   TRY_CUDA(h, cudaMemsetAsync(h->flag.p, 0, sizeof(int), st));
@@ -807,20 +812,22 @@ static int run_impl(mpgabor* h, const double* x_dev, int64_t Ls, int64_t maxit, 
   }
   if (coef_dev) TRY_CUDA(h, cudaMemsetAsync(coef_dev, 0, sizeof(double2) * h->P_R, st));
   TRY_CUDA(h, cudaEventRecord(h->ev[2], st));
-  std::vector<double> E0s(B, 0.0), Etols(B, 0.0);
-  int nonfinite = 0;
-  TRY_CUDA(h, cudaMemcpyAsync(E0s.data(), h->E0.p, sizeof(double) * B, cudaMemcpyDeviceToHost, st));
-  TRY_CUDA(h, cudaMemcpyAsync(&nonfinite, h->flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-  TRY_CUDA(h, cudaStreamSynchronize(st));
-  if (nonfinite) return h->fail(MPG_ENONFINITE, "x contains NaN or Inf");
-  // stop level 10^(errdb/10) E_0
-  for (int b = 0; b < B; ++b)
-    Etols[b] = etol_abs ? *etol_abs : (errdb == -INFINITY) ? -INFINITY : std::pow(10.0, errdb / 10.0) * E0s[b];
-  const double E0 = E0s[0], Etol = Etols[0];
-  TRY_CUDA(h, cudaMemcpyAsync(h->etolv.p, Etols.data(), sizeof(double) * B, cudaMemcpyHostToDevice, st));
+  // no host round trip before the loop: the loop kernel reads E_0 and the non-finite
+  // flag from the device and forms the stop level 10^(errdb/10) E_0 itself (P:340-341,
+  // P:1153); the one synchronisation is the result read-back after the loop
   P.nslot = B;
-  P.E0v = B > 1 ? h->E0.as<double>() : nullptr;
-  P.Etolv = B > 1 ? h->etolv.as<double>() : nullptr;
+  P.E0v = h->E0.as<double>();
+  P.nonfinite = h->flag.as<int>();
+  if (etol_abs) {
+    P.etol_mode = 2;
+    P.etol_val = *etol_abs;
+  } else if (errdb == -INFINITY) {
+    P.etol_mode = 0;
+    P.etol_val = 0.0;
+  } else {
+    P.etol_mode = 1;
+    P.etol_val = std::pow(10.0, errdb / 10.0);
+  }
   P.slot_grid = h->grid_elems;
   P.slot_atoms = maxit;
   P.dicts = h->d_geo.as<DictGeo>();
@@ -835,8 +842,7 @@ static int run_impl(mpgabor* h, const double* x_dev, int64_t Ls, int64_t maxit, 
   P.kern = h->kern.p;
   P.rec = h->rec.p;
   P.maxit = maxit;
-  P.Etol = Etol;
-  P.E0 = E0;
+  P.E0 = 0.0;
   P.atoms = reinterpret_cast<AtomOut*>(atoms_dev);
   P.energy = energy_dev;
   P.sol = reinterpret_cast<double2*>(coef_dev);
@@ -870,17 +876,17 @@ static int run_impl(mpgabor* h, const double* x_dev, int64_t Ls, int64_t maxit, 
   TRY_CUDA(h, cudaEventElapsedTime(&h->t_init, h->ev[1], h->ev[2]));
   TRY_CUDA(h, cudaEventElapsedTime(&h->t_loop, h->ev[3], h->ev[4]));
   if (P.prof) TRY_CUDA(h, cudaMemcpy(h->prof_host, P.prof, sizeof(long long) * MPG_PROF_SLOTS, cudaMemcpyDeviceToHost));
+  for (int b = 0; b < B; ++b)
+    if (lr[b].stop == STOP_NONFINITE) return h->fail(MPG_ENONFINITE, "x contains NaN or Inf");
   for (int b = 0; b < B; ++b) {
     res[b].n_atoms = lr[b].n_done;
     res[b].L_pad = h->L;
     res[b].stop_reason = lr[b].stop;
     res[b].cluster = h->lay_C;
-    res[b].E0 = E0s[b];
+    res[b].E0 = lr[b].E0;
     res[b].E_final = lr[b].E_final;
     res[b].rounds = h->kind == 2 ? lr[b].rounds : lr[b].n_done + 1;
   }
-  (void)E0;
-  (void)Etol;
   return MPG_OK;
 }
 
@@ -1055,8 +1061,16 @@ extern "C" int mpgabor_synth(mpgabor* h, const mpg_atom* atoms_dev, int64_t n_at
   for (auto& d : h->geo) fmax = std::max(fmax, (int64_t)d.N * d.M);
   TRY_CUDA(h, h->frames.ensure(sizeof(double) * fmax));
   TRY_CUDA(h, cudaMemsetAsync(h->sol.p, 0, sizeof(double2) * h->P_R, st));
-  TRY_LAUNCH(h, (n_atoms > 0 ? 1 : 0), launch_synth_scatter(reinterpret_cast<const AtomOut*>(atoms_dev), n_atoms, h->d_geo.as<DictGeo>(), h->W,
-                                   h->sol.as<double2>(), st));
+  if (n_atoms > 0) {
+    TRY_CUDA(h, h->sfirst.ensure(sizeof(unsigned int) * h->P_R));
+    TRY_CUDA(h, h->sdone.ensure((size_t)(n_atoms + 3) / 4 * 4 + 16));
+    TRY_CUDA(h, cudaMemsetAsync(h->sfirst.p, 0xff, sizeof(unsigned int) * h->P_R, st));
+    TRY_CUDA(h, cudaMemsetAsync(h->sdone.p, 0, (size_t)(n_atoms + 3) / 4 * 4 + 16, st));
+  }
+  TRY_LAUNCH(h, (n_atoms > 0 ? 1 : 0),
+             launch_synth_scatter(reinterpret_cast<const AtomOut*>(atoms_dev), n_atoms, h->d_geo.as<DictGeo>(), h->W,
+                                  h->sol.as<double2>(), h->sfirst.as<unsigned int>(), h->sdone.as<unsigned char>(),
+                                  reinterpret_cast<unsigned int*>(h->sdone.as<unsigned char>() + (n_atoms + 3) / 4 * 4), st));
   for (int w = 0; w < h->W; ++w) {
     const DictGeo& d = h->geo[w];
     TRY_LAUNCH(h, 1, launch_synth_frames(h->sol.as<double2>(), d, h->tw.as<double2>(), h->twres, h->frames.as<double>(), st));

@@ -8,14 +8,61 @@
 #include "launch.h"
 #include "fft.cuh"
 
+// Deterministic scatter of the atom list into the solution grid: sol(p) = 0 + c~_i1 +
+// c~_i2 + ... over the atoms selecting p, in atom-list order -- the order of Alg. 1 step 2a
+// (reading Z19) and of the oracle.  Rounds of one cooperative launch: every
+// pending atom offers its list index to first[p] (atomicMin, an order-free result); the
+// atom holding first[p] adds itself (one writer per p per round) and retires.  A p
+// selected m times takes m rounds; the sum order never depends on scheduling.
+__device__ __forceinline__ void synth_grid_barrier(unsigned int* ctr, unsigned int target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    unsigned int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
+
 __global__ void synth_scatter_kernel(const AtomOut* __restrict__ atoms, int64_t n, const DictGeo* __restrict__ dg,
-                                     double2* __restrict__ sol) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const AtomOut a = atoms[i];
-    const DictGeo d = dg[a.w];
-    double* s = reinterpret_cast<double*>(sol + d.off + (int64_t)a.n * d.MR + a.m);
-    atomicAdd(s, a.re);
-    if (a.im != 0.0) atomicAdd(s + 1, a.im);
+                                     double2* __restrict__ sol, unsigned int* __restrict__ first,
+                                     unsigned char* __restrict__ done, unsigned int* __restrict__ ctl) {
+  // ctl[0] barrier counter, ctl[1..2] "atoms left" flags of alternate rounds (all zero at launch)
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned int gen = 0;
+  for (int round = 0;; ++round) {
+    if (i0 == 0) ctl[1 + ((round + 1) & 1)] = 0;  // next round's flag (last read before this round)
+    for (int64_t i = i0; i < n; i += stride) {
+      if (done[i]) continue;
+      const AtomOut a = atoms[i];
+      const DictGeo d = dg[a.w];
+      atomicMin(first + d.off + (int64_t)a.n * d.MR + a.m, (unsigned int)i);
+    }
+    synth_grid_barrier(ctl, ++gen * gridDim.x);
+    bool left = false;
+    for (int64_t i = i0; i < n; i += stride) {
+      if (done[i]) continue;
+      const AtomOut a = atoms[i];
+      const DictGeo d = dg[a.w];
+      const int64_t p = d.off + (int64_t)a.n * d.MR + a.m;
+      if (first[p] == (unsigned int)i) {
+        double2 c = sol[p];
+        c.x += a.re;
+        c.y += a.im;
+        sol[p] = c;
+        first[p] = 0xffffffffu;
+        done[i] = 1;
+      } else {
+        left = true;
+      }
+    }
+    if (__syncthreads_or(left) && threadIdx.x == 0) ctl[1 + (round & 1)] = 1;
+    synth_grid_barrier(ctl, ++gen * gridDim.x);
+    if (*(volatile unsigned int*)&ctl[1 + (round & 1)] == 0) break;
   }
 }
 
@@ -81,12 +128,21 @@ __global__ void synth_ola_kernel(const double* __restrict__ frames, int a, int M
 }
 
 cudaError_t launch_synth_scatter(const AtomOut* atoms, int64_t n_atoms, const DictGeo* dg_dev, int W, double2* sol,
-                                 cudaStream_t st) {
+                                 unsigned int* first, unsigned char* done, unsigned int* ctl, cudaStream_t st) {
   (void)W;
   if (n_atoms <= 0) return cudaSuccess;
-  const int blocks = (int)std::min<int64_t>(1184, (n_atoms + 255) / 256);
-  synth_scatter_kernel<<<blocks, 256, 0, st>>>(atoms, n_atoms, dg_dev, sol);
-  return cudaGetLastError();
+  // co-resident CTAs (cooperative launch): at most the occupancy limit, at least one
+  static int maxb = 0;
+  if (maxb == 0) {
+    int per_sm = 0, dev = 0, sms = 0;
+    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, synth_scatter_kernel, 256, 0));
+    CUDA_OK(cudaGetDevice(&dev));
+    CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    maxb = std::max(1, std::min(per_sm, 4) * sms);
+  }
+  const int blocks = (int)std::min<int64_t>(maxb, (n_atoms + 255) / 256);
+  void* args[] = {(void*)&atoms, (void*)&n_atoms, (void*)&dg_dev, (void*)&sol, (void*)&first, (void*)&done, (void*)&ctl};
+  return cudaLaunchCooperativeKernel((const void*)synth_scatter_kernel, dim3(blocks), dim3(256), args, 0, st);
 }
 
 cudaError_t launch_synth_frames(const double2* sol, const DictGeo& d, const double2* tw, int twres, double* frames,

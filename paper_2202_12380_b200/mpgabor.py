@@ -56,7 +56,7 @@ _SIGS = {
     "mpgabor_create": ([ctypes.POINTER(mpg_dict), _I32, _I32, ctypes.POINTER(_P)], ctypes.c_int),
     "mpgabor_kernels": ([_P, ctypes.c_double, _P], ctypes.c_int),
     "mpgabor_layout": ([_P, _I64, ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I64),
-                        ctypes.POINTER(_I64)], ctypes.c_int),
+                        ctypes.POINTER(_I64), ctypes.POINTER(_I64)], ctypes.c_int),
     "mpgabor_run": ([_P, _P, _I64, _I64, ctypes.c_double, _P, _P, _P, ctypes.POINTER(mpg_result), _P],
                     ctypes.c_int),
     "mpgabor_synth": ([_P, _P, _I64, _P, _I64, _P], ctypes.c_int),
@@ -135,12 +135,14 @@ def mpgabor_kernels(h, thr, stream=None):
 
 
 def mpgabor_layout(h, Ls, W):
+    """(L_pad, N[W], M_R[W], coef_offset[W+1], row_stride[W])."""
     L = _I64()
     N = (_I64 * W)()
     MR = (_I64 * W)()
+    rs = (_I64 * W)()
     off = (_I64 * (W + 1))()
-    _check(h, _lib.mpgabor_layout(h, int(Ls), ctypes.byref(L), N, MR, off))
-    return L.value, list(N), list(MR), list(off)
+    _check(h, _lib.mpgabor_layout(h, int(Ls), ctypes.byref(L), N, MR, rs, off))
+    return L.value, list(N), list(MR), list(off), list(rs)
 
 
 def mpgabor_run(h, x_dev, Ls, maxit, errdb, atoms_dev, energy_dev, coef_dev=None, stream=None):

@@ -65,9 +65,10 @@ def test_create_accepts_and_layout_matches_oracle(mpg):
         cfg = CONFIGS[name]
         h = mpg.mpgabor_create(cfg.dicts, mpg.MPG_F64)
         try:
-            L, N, MR, off = mpg.mpgabor_layout(h, cfg.Ls, len(cfg.dicts))
+            L, N, MR, off, rs = mpg.mpgabor_layout(h, cfg.Ls, len(cfg.dicts))
             lay = gabor.layout(cfg.dicts, cfg.Ls)
             assert L == lay.L and N == lay.N and MR == lay.MR and off[:-1] == lay.off and off[-1] == lay.P
+            assert rs == lay.MR        # exchanged coefficient vectors are dense (row stride M_R)
         finally:
             mpg.mpgabor_destroy(h)
 

@@ -46,8 +46,6 @@ for name in cfgs:
         print(f"   per-CTA busy cycles/round (receive -> publish) over {Cn} CTAs: mean {sum(busy) / Cn:.0f} "
               f"min {min(busy):.0f} max {max(busy):.0f}; items/round mean {sum(items) / Cn:.2f} "
               f"min {min(items):.2f} max {max(items):.2f}", flush=True)
-        if c[19]:
-            print(f"   thread-0 items: {c[19]} ({c[19] / n:.2f}/round) setup {c[16] / c[19]:.0f} loads {c[17] / c[19]:.0f} "
-                  f"update+bookkeeping {c[18] / c[19]:.0f} cycles/item", flush=True)
+        print(f"   candidate-list rebuilds: {c[19]} ({100 * c[19] / n:.2f} % of rounds)", flush=True)
         mp.set_profile(0)
     mp.close()
