@@ -47,7 +47,11 @@ enum { MPG_F64 = 0, MPG_F32 = 1 };
 /* one Gabor dictionary: window kind, window length gl, hop a, channels M
  * (dgtrealmp_parbuf_add_firwin(win, gl, a, M)).  Requirements:
  * M a power of two with 2 <= M <= 16384, a >= 1, M % a == 0,
- * gl >= 1. */
+ * gl >= 1.  The paper only needs pairwise divisibility; the power-of-two
+ * M is this library's deliberate restriction (Z25): it covers every
+ * configuration of the paper's experiments and lets the DGT and
+ * synthesis use radix-2 shared-memory FFTs and the loop kernels shift/mask index
+ * arithmetic; other M are rejected with MPG_EINVAL. */
 typedef struct {
   int32_t win, gl, a, M;
 } mpg_dict;

@@ -668,8 +668,11 @@ __device__ __forceinline__ unsigned long long gx_ld_acquire(const unsigned long 
 // identical.
 // TOPK: how a CTA finds its K best tiles each round -- 0 down the 32-ary node tree, 1 by a
 // scan of all its tile records, 2 from its candidate list (ClState).
+#ifndef MPG_LB_THREADS
+#define MPG_LB_THREADS 512  // launch bound (max threads per CTA; 256 leaves 255 registers per thread)
+#endif
 template <typename R, int TW, bool SREC, int K, bool GX, int TOPK = 0>
-__global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
+__global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopParams P) {
   using C2 = typename cplx<R>::t;
   using RecT = Rec<R>;
   using MsgT = Msg<R, K>;
@@ -681,7 +684,7 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
   constexpr int NCH = TW / 32;
   constexpr int TPI = tiles_per_item<TW>();
   constexpr bool notree = TOPK != 0;  // top-K without the node tree (no tree upkeep per round)
-  static_assert(TOPK == 0 || SREC, "the scan / list top-K read shared-memory tile records");
+  static_assert(TOPK != 1 || SREC, "the scan top-K reads shared-memory tile records");
   const int NEc = min(NE, C * K);
   const int B = max(1, min(BMAX, P.spec));
 
@@ -1464,18 +1467,13 @@ __global__ void __launch_bounds__(512, 1) mp_multi_kernel(const LoopParams P) {
       // at 128 registers and was slower: C2 2.24 vs 1.93 us/atom)
       constexpr int IF = NCH == 1 ? MPG_ITEMS_IN_FLIGHT : 1;
       for (int gi = lo + warp; gi < hi; gi += IF * NW) {
-        if constexpr (IF == 2) {
-          ItemS A, B;
-          const bool hasB = gi + NW < hi;
-          setup(gi, A);
-          if (hasB) setup(gi + NW, B);
-          process(A);
-          if (hasB) process(B);
-        } else {
-          ItemS A;
-          setup(gi, A);
-          process(A);
-        }
+        ItemS A[IF];
+#pragma unroll
+        for (int f = 0; f < IF; ++f)   // every item's loads in flight before the first update
+          if (gi + f * NW < hi) setup(gi + f * NW, A[f]);
+#pragma unroll
+        for (int f = 0; f < IF; ++f)
+          if (gi + f * NW < hi) process(A[f]);
       }
     } else {
       // roll back the rejected candidates' tiles from their backups
@@ -1660,16 +1658,16 @@ int max_grid_t(int threads, size_t smem) {
 
 template <typename R, bool SREC, bool GX>
 cudaError_t launch_r(const LoopParams& P, int threads, cudaStream_t st) {
+  if (P.topk_scan == 2) switch (P.TW) {  // candidate lists (records in shared or global memory)
+      case 32: return launch_t<R, 32, SREC, MULTI_K, GX, 2>(P, threads, st);
+      case 64: return launch_t<R, 64, SREC, MULTI_K, GX, 2>(P, threads, st);
+      case 128: return launch_t<R, 128, SREC, MULTI_K, GX, 2>(P, threads, st);
+    }
   if constexpr (SREC && !GX) {
     if (P.topk_scan == 1) switch (P.TW) {
         case 32: return launch_t<R, 32, true, MULTI_K, false, 1>(P, threads, st);
         case 64: return launch_t<R, 64, true, MULTI_K, false, 1>(P, threads, st);
         case 128: return launch_t<R, 128, true, MULTI_K, false, 1>(P, threads, st);
-      }
-    if (P.topk_scan == 2) switch (P.TW) {
-        case 32: return launch_t<R, 32, true, MULTI_K, false, 2>(P, threads, st);
-        case 64: return launch_t<R, 64, true, MULTI_K, false, 2>(P, threads, st);
-        case 128: return launch_t<R, 128, true, MULTI_K, false, 2>(P, threads, st);
       }
   }
   switch (P.TW) {

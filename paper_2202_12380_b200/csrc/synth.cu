@@ -20,8 +20,10 @@ __device__ __forceinline__ void synth_grid_barrier(unsigned int* ctr, unsigned i
     __threadfence();
     atomicAdd(ctr, 1u);
     unsigned int v;
+    const long long t0 = clock64();
     do {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+      if (clock64() - t0 > (1LL << 35)) __trap();  // a CTA that never arrives: fail, do not hang
     } while (v < target);
   }
   __syncthreads();
@@ -30,12 +32,13 @@ __device__ __forceinline__ void synth_grid_barrier(unsigned int* ctr, unsigned i
 __global__ void synth_scatter_kernel(const AtomOut* __restrict__ atoms, int64_t n, const DictGeo* __restrict__ dg,
                                      double2* __restrict__ sol, unsigned int* __restrict__ first,
                                      unsigned char* __restrict__ done, unsigned int* __restrict__ ctl) {
-  // ctl[0] barrier counter, ctl[1..2] "atoms left" flags of alternate rounds (all zero at launch)
+  // ctl[0] barrier counter, ctl[1 + r % 3] "atoms left" flag of round r (all zero at launch):
+  // round r clears the slot of round r + 1, last read (by every CTA) before round r - 1 ended
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   unsigned int gen = 0;
   for (int round = 0;; ++round) {
-    if (i0 == 0) ctl[1 + ((round + 1) & 1)] = 0;  // next round's flag (last read before this round)
+    if (i0 == 0) ctl[1 + (round + 1) % 3] = 0;
     for (int64_t i = i0; i < n; i += stride) {
       if (done[i]) continue;
       const AtomOut a = atoms[i];
@@ -60,9 +63,9 @@ __global__ void synth_scatter_kernel(const AtomOut* __restrict__ atoms, int64_t 
         left = true;
       }
     }
-    if (__syncthreads_or(left) && threadIdx.x == 0) ctl[1 + (round & 1)] = 1;
+    if (__syncthreads_or(left) && threadIdx.x == 0) ctl[1 + round % 3] = 1;
     synth_grid_barrier(ctl, ++gen * gridDim.x);
-    if (*(volatile unsigned int*)&ctl[1 + (round & 1)] == 0) break;
+    if (*(volatile unsigned int*)&ctl[1 + round % 3] == 0) break;
   }
 }
 

@@ -88,11 +88,22 @@ for name in cfgs:
             row["argmax_us_per_it"] = us_it * (1 - share)
             row["update_gbs"] = row["alg_bytes_per_it"] / (row["update_us_per_it"] * 1e-6) / 1e9
             row["update_roofline_frac"] = row["update_gbs"] / peak
-            if kernel == "mp_loop_kernel":   # latency floor: same loop, update skipped
-                mp.set_profile(2)
-                rf, _ = mp.run(xd, n, -float("inf"), bufs=bufs, fetch=False)
-                row["floor_us_per_it"] = 1e3 * mp.last_timing()[2] / max(rf.n_atoms, 1)
-                mp.set_profile(0)
+            # latency floor (profile mode bit 1): the same loop kernel and launch with the
+            # update skipped -- one-selection: the per-iteration exchange/selection chain;
+            # multi-selection: rounds of one atom with no items (the fixed cost of a round),
+            # scaled by the real run's rounds.  Warm, median of the runs.
+            mp.set_profile(2)
+            nf = n if kernel == "mp_loop_kernel" else int(out.rounds)
+            mp.run(xd, nf, -float("inf"), bufs=bufs, fetch=False)
+            fl = []
+            for _ in range(runs):
+                rf, _ = mp.run(xd, nf, -float("inf"), bufs=bufs, fetch=False)
+                fl.append(mp.last_timing()[2] / max(rf.n_atoms, 1))
+            mp.set_profile(0)
+            per = float(np.median(fl)) * 1e3          # us per floor iteration / round
+            row["floor_us_per_round"] = per
+            row["floor_us_per_it"] = per * (1.0 if kernel == "mp_loop_kernel" else out.rounds / max(n, 1))
+            row["floor_frac"] = row["floor_us_per_it"] / us_it
             rows.append(row)
             print(json.dumps(row), flush=True)
         mp.close()
@@ -105,12 +116,13 @@ with open(f"profiles/{tag}_configs.md", "w") as f:
             "8 = exact multi-selection.  Loop only (DGT separate); median of the runs.  Update/argmax split "
             "from CTA 0's per-phase clock64 sums.  Roofline = algorithmic update bytes / time / peak.\n\n")
     f.write("| config | prec | batch | kernel | CTAs | TW | atoms | rounds | it/s | us/it | touched/it | GB/s | frac | "
-            "update us/it | update frac | argmax us/it | floor us/it | DGT ms |\n")
-    f.write("|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|\n")
+            "update us/it | update frac | argmax us/it | floor us/it | floor frac | DGT ms |\n")
+    f.write("|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|\n")
     for r in rows:
         fl = r.get("floor_us_per_it")
         f.write(f"| {r['config']} | {r['precision']} | {r['batch']} | {r['kernel']} | {r['launch']['cluster']} | {r['launch']['tile_width']} | {r['atoms']} | {r['rounds']} | "
                 f"{r['it_per_s']:.0f} | {r['us_per_it']:.3f} | {r['touched_per_it']:.0f} | {r['achieved_gbs']:.1f} | "
                 f"{r['roofline_frac']:.4f} | {r['update_us_per_it']:.3f} | {r['update_roofline_frac']:.4f} | "
-                f"{r['argmax_us_per_it']:.3f} | {'' if fl is None else f'{fl:.3f}'} | {r['dgt_ms']:.2f} |\n")
+                f"{r['argmax_us_per_it']:.3f} | {'' if fl is None else f'{fl:.3f}'} | "
+                f"{r.get('floor_frac', float('nan')):.2f} | {r['dgt_ms']:.2f} |\n")
 print("wrote", f"profiles/{tag}_configs.md")
