@@ -664,7 +664,7 @@ static int ensure_layout(mpgabor* h, int64_t Ls) {
   // record (1); env MPGABOR_TOPK = 0/1/2 overrides, for measurements
   {
     const char* ev = std::getenv("MPGABOR_TOPK");
-    const int want = ev ? std::atoi(ev) : (h->srec ? 2 : 0);
+    const int want = ev ? std::atoi(ev) : 2;
     P.topk_scan = h->kind == 2 ? std::max(0, std::min(2, want)) : 0;
     if ((h->gx || !h->srec) && P.topk_scan == 1) P.topk_scan = 0;  // (scan: shared records of a cluster)
     if (P.topk_scan) {  // the list's shared memory (membership flags per record) must fit

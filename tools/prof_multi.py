@@ -46,6 +46,7 @@ for name in cfgs:
         print(f"   per-CTA busy cycles/round (receive -> publish) over {Cn} CTAs: mean {sum(busy) / Cn:.0f} "
               f"min {min(busy):.0f} max {max(busy):.0f}; items/round mean {sum(items) / Cn:.2f} "
               f"min {min(items):.2f} max {max(items):.2f}", flush=True)
-        print(f"   candidate-list rebuilds: {c[19]} ({100 * c[19] / n:.2f} % of rounds)", flush=True)
+        print(f"   candidate-list rebuilds: {c[19]} ({100 * c[19] / n:.2f} % of rounds), "
+              f"{c[17] / max(c[19], 1):.0f} cycles each; extraction {c[16] / n:.0f} cycles/round", flush=True)
         mp.set_profile(0)
     mp.close()
