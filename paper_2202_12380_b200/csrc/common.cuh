@@ -89,6 +89,25 @@ MPG_HD int ilog2(int x) {  // x a power of two
 template <typename S, typename P>
 MPG_HD bool better(S s1, P p1, S s2, P p2) { return s1 > s2 || (s1 == s2 && p1 < p2); }
 
+// Debug builds (-DMPG_CHECKS, tools/build_variant.sh): device-side protocol and bounds
+// checks that trap with a message (the launch then fails with a CUDA error).  They stand
+// in for compute-sanitizer, which this GPU pool does not offer.
+#ifdef MPG_CHECKS
+#include <cstdio>
+#define MPG_CHECK(cond, what)                                                                              \
+  do {                                                                                                     \
+    if (!(cond)) {                                                                                         \
+      printf("MPG_CHECK failed: %s (%s:%d) block %d thread %d\n", what, __FILE__, __LINE__, (int)blockIdx.x, \
+             (int)threadIdx.x);                                                                            \
+      __trap();                                                                                            \
+    }                                                                                                      \
+  } while (0)
+#else
+#define MPG_CHECK(cond, what) \
+  do {                        \
+  } while (0)
+#endif
+
 #define CUDA_OK(x)                                   \
   do {                                               \
     cudaError_t e_ = (x);                            \

@@ -70,6 +70,7 @@ struct LoopParams {
   const int* rho_off;            // [W]
   void* grid;                    // residual grids (cplx<R>)
   const void* kern;              // kernels (cplx<R>), per-class layout
+  long long kern_elems;          // kernel entries (bounds checks of debug builds)
   void* rec;                     // Rec<R>[C * Lc] (initial records; the live ones when !srec)
   long long maxit;
   double E0;

@@ -83,6 +83,9 @@ template <typename R, int K>
 struct Msg {              // published by every CTA to every CTA at the end of a round
   Rec<R> list[K];         // its K best tile records, (score desc, index asc)
   uint32_t vkey[BMAX];    // per candidate: max score key over the candidate's tiles owned by the CTA
+#ifdef MPG_CHECKS
+  uint32_t tag, pad_[3];  // debug builds: the round stamp the message was published with
+#endif
 };
 
 struct Ent {              // one merged list entry of the walk window
@@ -815,6 +818,9 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
   // `slot` of every CTA
   auto publish = [&](int ps, unsigned long long stamp) {
     if (lane < K) mymsg->list[lane] = tk[lane] >= 0 ? trec[tk[lane]] : empty_rec(R(0));
+#ifdef MPG_CHECKS
+    if (lane == 0) mymsg->tag = (uint32_t)stamp;
+#endif
     if (lane < BMAX) {
       mymsg->vkey[lane] = vkey[lane];
       vkey[lane] = 0;
@@ -911,6 +917,10 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
       if (P.prof != nullptr && slot == 0 && tid == 0) tbusy0 = clock64();
       PROF_MARK(0);
       if (!GX && lane == 0) mbar_arm(smem_addr(&mbar[par]), C * msgbytes);  // slot reused at round + 2
+#ifdef MPG_CHECKS
+      for (int c = lane; c < C; c += 32)   // every message is the one published for this round
+        MPG_CHECK(mb[c].tag == (uint32_t)round + 1u, "mailbox message from another round");
+#endif
       const int Gp = st->G;
       int acc = Gp;
       if (Gp >= 2) {
@@ -1360,6 +1370,7 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
         rec.im = bim;
         rec.p = bp;
         if constexpr (sizeof(R) == 8) rec.pad = 0;
+        MPG_CHECK(l >= 0 && l < P.Lc && g >= 0 && g < BMAX, "tile record / candidate index out of range");
         trec[l] = rec;
         if constexpr (decltype(upd)::value) atomicMax(&vkey[g], score_key(bs));
         if constexpr (TOPK == 2) {  // a rewritten tile at or above theta joins the candidate list
@@ -1415,7 +1426,12 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
       const int r = i < gg.cntA ? gg.rhoA + (i << lgC) : gg.rA + gg.rhoB + ((i - gg.cntA) << lgC);
       int nrow = gg.n0 + r;
       if (nrow >= dv.N) nrow -= dv.N;
+      MPG_CHECK(nrow >= 0 && nrow < dv.N && r >= 0 && r < gg.nr, "item row outside the target grid");
+      MPG_CHECK(((dv.frame_off + nrow) & (C - 1)) == rank, "item row not owned by this CTA");
       S.l0 = sown[v].loc_base + ((nrow - sown[v].n_first) >> lgC) * dv.T;
+      MPG_CHECK(S.l0 >= 0 && S.l0 + t0 + Tr <= P.Lc, "tile record index out of range");
+      MPG_CHECK(st->tbase[gv] + (long long)(i + 1) * Tr <= P.bk_cap, "backup slot out of range");
+      MPG_CHECK(gg.kbase + (long long)(r + 1) * gg.nc <= P.kern_elems, "kernel row out of range");
       S.row = grid + dv.grid_off + (long long)nrow * dv.stride;
       S.bkrow = backup + ((long long)st->tbase[gv] + (long long)i * Tr) * TW;
       S.pbase = (uint32_t)dv.off + (uint32_t)nrow * (uint32_t)MR;
@@ -1439,6 +1455,7 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
         for (int ch = 0; ch < NCH; ++ch) {  // issue every load before any store
           const int bin = (t0 + tt + q) * TW + ch * 32 + lane;
           const bool valid = (tt + q < Tr) && bin < MR;
+          MPG_CHECK(!valid || bin < dv.stride, "bin outside the row stride");
           const int cd = (bin - q0) & (Mv - 1);   // direct source column  (q = bin)
           const int cc = (-bin - q0) & (Mv - 1);  // conjugate source column (q = M - bin)
           S.fd[q][ch] = valid && cd < nc;

@@ -841,6 +841,7 @@ static int run_impl(mpgabor* h, const double* x_dev, int64_t Ls, int64_t maxit, 
   P.rho_off = h->rho_meta.as<int>() + 2 * W;
   P.grid = h->grid.p;
   P.kern = h->kern.p;
+  P.kern_elems = h->kern_elems;
   P.rec = h->rec.p;
   P.maxit = maxit;
   P.E0 = 0.0;
