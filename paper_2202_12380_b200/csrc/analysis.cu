@@ -91,30 +91,40 @@ __global__ void sum_partials_kernel(const double* __restrict__ partial, int n, d
 // F frames per CTA.  Output row stride `stride` (>= M/2+1, zero padded).
 // ---------------------------------------------------------------------------
 template <typename R>
-__global__ void dgt_kernel(const double* __restrict__ x, int64_t L, int a, int M, int gl, int N,
-                           const double* __restrict__ g, const double2* __restrict__ tw, int twres,
-                           typename cplx<R>::t* __restrict__ out, int stride, int F) {
+__global__ void __launch_bounds__(1024) dgt_kernel(const double* __restrict__ x, int64_t L, int a, int M, int gl, int N,
+                                                   const double* __restrict__ g, const double2* __restrict__ tw,
+                                                   int twres, typename cplx<R>::t* __restrict__ out, int stride, int F,
+                                                   uint32_t stride_magic) {
   using C2 = typename cplx<R>::t;
   extern __shared__ double2 z[];
   const int n = M / 2;
-  const int lgn = 31 - __clz(n);
+  const int lgn = 31 - __clz(n), lgM = lgn + 1;
   const int j0 = -(gl / 2);
   const int frame0 = blockIdx.x * F;
-  for (int idx = threadIdx.x; idx < F * M; idx += blockDim.x) {
-    const int f = idx / M, s = idx - f * M;
+  // fold the windowed frame modulo M (M a power of two: masks, no integer division;
+  // sample positions wrap circularly by one conditional add / subtract of L)
+  for (int idx = threadIdx.x; idx < F << lgM; idx += blockDim.x) {
+    const int f = idx >> lgM, s = idx & (M - 1);
     const int frame = frame0 + f;
     double v = 0.0;
     if (frame < N) {
       const int64_t base = (int64_t)frame * a;
-      for (int j = j0 + fmod32(s - j0, M); j < j0 + gl; j += M) v += x[fmod64(base + j, L)] * g[j - j0];
+      for (int j = j0 + ((s - j0) & (M - 1)); j < j0 + gl; j += M) {
+        int64_t pos = base + j;
+        pos += pos < 0 ? L : 0;
+        pos -= pos >= L ? L : 0;
+        v += x[pos] * g[j - j0];
+      }
     }
     double* zz = reinterpret_cast<double*>(&z[f * n + bitrev(s >> 1, lgn)]);
     zz[s & 1] = v;
   }
   __syncthreads();
   smem_fft(z, lgn, F, tw, twres, -1);
+  // row f of the output: bins 0..n, then zero padding up to the row stride;
+  // f = idx / stride by a multiply-high with the host's magic (exact for idx < 2^16)
   for (int idx = threadIdx.x; idx < F * stride; idx += blockDim.x) {
-    const int f = idx / stride, m = idx - f * stride;
+    const int f = (int)__umulhi((uint32_t)idx, stride_magic), m = idx - f * stride;
     const int frame = frame0 + f;
     if (frame >= N) continue;
     C2 o;
@@ -342,19 +352,26 @@ cudaError_t launch_pad_energy(const double* x, int64_t Ls, double* xp, int64_t L
   return cudaGetLastError();
 }
 
-static int dgt_frames_per_cta(int M) { return max(1, 2048 / (M / 2)); }
+// frames per CTA: 4096 complex values of shared memory (64 KB) per CTA, threads up to
+// 1024 so that a large-M transform (one frame) still has every SM busy
+static int dgt_frames_per_cta(int M) { return max(1, 4096 / (M / 2)); }
 
 template <typename R>
 cudaError_t launch_dgt(const double* xp, int64_t L, const DictGeo& d, const double* g, const double2* tw,
                        int twres, typename cplx<R>::t* out, cudaStream_t st) {
-  const int F = dgt_frames_per_cta(d.M);
+  // (F * stride < 2^16 keeps the output row index by multiply-high exact)
+  const int F = std::max(1, std::min(dgt_frames_per_cta(d.M), 65535 / d.stride));
   const size_t smem = (size_t)F * (d.M / 2) * sizeof(double2);
   static bool attr = false;
   if (!attr) {
     CUDA_OK(cudaFuncSetAttribute(dgt_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr = true;
   }
-  dgt_kernel<R><<<(d.N + F - 1) / F, 256, smem, st>>>(xp, L, d.a, d.M, d.gl, d.N, g, tw, twres, out, d.stride, F);
+  if ((int64_t)F * d.stride >= (1 << 16)) return cudaErrorInvalidValue;
+  const uint32_t magic = (uint32_t)((0x100000000ull + (uint64_t)d.stride - 1) / (uint64_t)d.stride);
+  const int threads = (int64_t)F * (d.M / 2) >= 8192 ? 1024 : 512;
+  dgt_kernel<R><<<(d.N + F - 1) / F, threads, smem, st>>>(xp, L, d.a, d.M, d.gl, d.N, g, tw, twres, out, d.stride, F,
+                                                          magic);
   return cudaGetLastError();
 }
 template cudaError_t launch_dgt<double>(const double*, int64_t, const DictGeo&, const double*, const double2*, int,

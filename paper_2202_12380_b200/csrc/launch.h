@@ -113,6 +113,7 @@ int loop_max_cluster(bool f64, bool srec, int TW, int threads, size_t smem, bool
 constexpr int MULTI_K = MPG_MULTI_K;
 size_t multi_smem_bytes(const LoopParams& P, bool f64);
 int multi_max_batch();
+int multi_max_threads();  // the multi-selection kernel's launch bound (MPG_LB_THREADS)
 cudaError_t launch_multi_loop(const LoopParams& P, bool f64, int threads, cudaStream_t st);
 // gx: the global-exchange grid kernel; returns its co-resident CTA count
 int multi_max_cluster(bool f64, bool srec, int TW, int threads, size_t smem, bool gx = false);

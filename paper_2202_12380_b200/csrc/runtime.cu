@@ -439,8 +439,8 @@ extern "C" int mpgabor_set_launch(mpgabor* h, int32_t cluster, int32_t threads, 
   if (!h) return MPG_EINVAL;
   if (cluster < 0 || cluster > 128 || (cluster && (cluster & (cluster - 1))))
     return h->fail(MPG_EINVAL, "cluster must be 0, a power of two <= 16 (one cluster) or 32/64/128 (grid)");
-  if (threads && (threads < 128 || threads > 512 || threads % 32))
-    return h->fail(MPG_EINVAL, "threads must be in [128,512], multiple of 32");
+  if (threads && (threads < 128 || threads > multi_max_threads() || threads % 32))
+    return h->fail(MPG_EINVAL, "threads must be in [128," + std::to_string(multi_max_threads()) + "], multiple of 32");
   if (tile_width && tile_width != 32 && tile_width != 64 && tile_width != 128)
     return h->fail(MPG_EINVAL, "tile width must be 32, 64 or 128");
   if (records < 0 || records > 2) return h->fail(MPG_EINVAL, "records must be 0 (auto), 1 (shared) or 2 (global)");
