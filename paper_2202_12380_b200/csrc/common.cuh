@@ -35,7 +35,7 @@ struct DictGeo {
   int32_t N, MR;          // frames L/a, reduced bins M/2+1
   int32_t T, stride;      // tiles per frame, padded row stride (= T*TW)
   int32_t frame_off;      // global frame id of frame 0 (frames of all dictionaries in order)
-  int32_t pad_;
+  uint32_t mr_magic;      // ceil(2^32 / MR): q / MR = umulhi(q, mr_magic) or one less (decode)
   int64_t off;            // global coefficient index of (n=0, m=0)
   int64_t grid_off;       // element offset of this dictionary in the padded grid
   int64_t tile_off;       // global tile id of (n=0, t=0)
@@ -55,8 +55,12 @@ struct PairGeo {          // u = selected dictionary, v = updated dictionary
   int32_t mu_lo, mu_hi, nu_lo, nu_hi;
   int32_t nmu, nnu;       // box size
   int32_t rstep;          // Rmax / R: index step into the common root table
+  int32_t sh;             // packed shifts (5 bits each, PG_SH_*): log2 a_c, s_m, s_n, M_c/M_u, a_u/a_c, a_v, a_u
   int64_t koff;           // element offset of this pair's kernel storage
 };
+
+enum { PG_SH_AC = 0, PG_SH_SM = 5, PG_SH_SN = 10, PG_SH_MCU = 15, PG_SH_AUC = 20, PG_SH_AV = 25 };
+MPG_HD int pg_sh(int32_t sh, int f) { return (sh >> f) & 31; }
 
 // Tile record: best |c|^2 of a tile with its global index and value.  Scores are
 // >= +0 so their IEEE bit patterns order like the values; an empty record is

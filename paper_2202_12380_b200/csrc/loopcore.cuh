@@ -182,14 +182,16 @@ __device__ __forceinline__ void target_hull(int q0, int nc, int M, int& bmin, in
 template <int LGTW>
 __device__ __forceinline__ int vgeo(const PairGeo& pg, const DictGeo& du, const DictGeo& dv, int k, int j, int rank,
                                     int C, int lgC, VGeo& g) {
-  const int lgac = ilog2(pg.a_c), lgsm = ilog2(pg.s_m), lgsn = ilog2(pg.s_n);
-  const int kp = k << (ilog2(pg.M_c) - ilog2(du.M));                       // k' = k M_c/M_u
-  const int on = (-(j << (ilog2(du.a) - lgac)) - pg.nu_lo) & (pg.s_n - 1);
+  // every stride is a power of two; the shifts come precomputed with the pair (PairGeo::sh)
+  const int lgac = pg_sh(pg.sh, PG_SH_AC), lgsm = pg_sh(pg.sh, PG_SH_SM), lgsn = pg_sh(pg.sh, PG_SH_SN);
+  const int lgauc = pg_sh(pg.sh, PG_SH_AUC);
+  const int kp = k << pg_sh(pg.sh, PG_SH_MCU);                              // k' = k M_c/M_u
+  const int on = (-(j << lgauc) - pg.nu_lo) & (pg.s_n - 1);
   const int om = (-kp - pg.mu_lo) & (pg.s_m - 1);
   g.nr = on < pg.nnu ? (pg.nnu - on + pg.s_n - 1) >> lgsn : 0;
   g.nc = om < pg.nmu ? (pg.nmu - om + pg.s_m - 1) >> lgsm : 0;
-  const int tnum = (j << ilog2(du.a)) + ((pg.nu_lo + on) << lgac);          // divisible by a_v
-  int n0 = tnum >> ilog2(dv.a);
+  const int tnum = ((j << lgauc) + pg.nu_lo + on) << lgac;                  // divisible by a_v
+  int n0 = tnum >> pg_sh(pg.sh, PG_SH_AV);
   if (n0 < 0) n0 += dv.N;
   if (n0 >= dv.N) n0 -= dv.N;
   g.n0 = n0;

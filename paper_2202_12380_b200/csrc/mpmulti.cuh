@@ -120,7 +120,7 @@ struct TkE {              // a top-K candidate: order key, index, id (tile; -1 =
 
 struct Smem {
   size_t mbar, mail, mymsg, trec, lev, ent, egeo, wmask, rect, ecnt, st, vkey, sorted, hsel, tk, wk, stamp, list, cnt, pairs, dicts, own, roots,
-      rho, rho_meta, cls, clid, hist, inl, hk, nmax, total;
+      rho, rho_meta, cls, clid, hist, inl, rcp, hk, nmax, total;
 };
 
 // Candidate list of a CTA (top-K mode 2): the tiles whose score key is >= theta, held
@@ -147,6 +147,8 @@ struct ClState {
 };
 
 __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+// items per row hp = ceil(hull tiles / tiles per item) <= ceil(257 / 2) (M <= 16384, TW >= 32)
+constexpr int RCP_N = 256;
 
 
 __host__ __device__ inline Smem smem_layout(const LoopParams& P, size_t recsz, size_t msgsz) {
@@ -225,6 +227,8 @@ __host__ __device__ inline Smem smem_layout(const LoopParams& P, size_t recsz, s
   s.inl = o;
   o += P.topk_scan == 2 ? (size_t)P.Lc : 0;
   o = align_up(o, 16);
+  s.rcp = o;                  // 0xFFFFFFFF / h + 1 for h < RCP_N (items per row -> row index by umulhi)
+  o += sizeof(uint32_t) * RCP_N;
   s.hk = o;                   // candidate lists: upper 32 bits of every tile's score key
   o += P.topk_scan == 2 ? sizeof(uint32_t) * (size_t)P.Lc : 0;
   s.nmax = o;                 // candidate lists: node maxima of hk (rebuilds)
@@ -629,8 +633,12 @@ __device__ __forceinline__ void decode_p(uint32_t p, const DictGeo* sd, int W, i
   for (int w = 1; w < W; ++w) u += (uint32_t)sd[w].off <= p ? 1 : 0;
   const uint32_t q = p - (uint32_t)sd[u].off;
   const int MR = sd[u].MR;
-  j = (int)(q / (uint32_t)MR);
-  k = (int)(q - (uint32_t)j * (uint32_t)MR);
+  // q / MR by the rounded-up reciprocal: umulhi gives the quotient or one more
+  uint32_t jq = __umulhi(q, sd[u].mr_magic);
+  int r = (int)(q - jq * (uint32_t)MR);
+  jq = r < 0 ? jq - 1u : jq;
+  j = (int)jq;
+  k = r < 0 ? r + MR : r;
 }
 
 // packed rect of the tiles an update touches in one target dictionary:
@@ -727,6 +735,7 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
   unsigned char* inl = smem + L.inl;
   uint32_t* hk = reinterpret_cast<uint32_t*>(smem + L.hk);
   uint32_t* nmx = reinterpret_cast<uint32_t*>(smem + L.nmax);
+  uint32_t* rcp = reinterpret_cast<uint32_t*>(smem + L.rcp);
   // batched independent signals: cluster `slot` works on signal `slot` (its own grids,
   // records, backups, atoms, energies, result; the kernels are shared)
   const int slot = GX ? 0 : (int)(blockIdx.x / (unsigned)C);
@@ -767,6 +776,7 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
     for (int l = 0; l < P.nlev; ++l) levtot += P.lev_n[l];
     for (int i = tid; i < levtot; i += blockDim.x) stamp[i] = 0;
   }
+  for (int i = tid; i < RCP_N; i += blockDim.x) rcp[i] = i > 1 ? 0xFFFFFFFFu / (uint32_t)i + 1u : 0u;
   if (tid < MAX_LEVELS) cnt[tid] = 0;
   if (tid < BMAX) vkey[tid] = 0;
   if (SREC)
@@ -1042,25 +1052,43 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
       if constexpr (GX) {
         // stage 2 (warp 0): the K entries of each selected list, one per lane, ranked
         // among themselves -- exact, since every entry ahead of one of them is one of them
-        static_assert(NE * K <= 32, "stage-2 candidates fit one warp");
+        constexpr int S2 = (NE * K + 31) / 32;   // stage-2 entries per lane
+        static_assert(S2 <= 2, "stage-2 candidates fit one warp, two per lane");
         if (warp == 0) {
-          const bool have = lane < NEc * K;
-          const int hs = have ? hsel[lane / K] : -1;
-          const bool hv = hs >= 0;   // (always: C >= 32 > NE lists, empty ones included)
-          const int cl = hv ? hs : 0, q = lane % K;
-          const int e = cl * K + q;
-          const uint64_t ke = hv ? skey64(mb[cl].list[q].s) : 0ull;
-          const uint32_t pe = hv ? mb[cl].list[q].p : NO_INDEX;
-          int cnt = 0;
-#pragma unroll 8
-          for (int j = 0; j < 32; ++j) {
-            const uint64_t kf = __shfl_sync(0xffffffffu, ke, j);
-            const uint32_t pf = __shfl_sync(0xffffffffu, pe, j);
-            const int ef = __shfl_sync(0xffffffffu, e, j);
-            const bool ahead = (kf > ke) | ((kf == ke) & ((pf < pe) | ((pf == pe) & (ef < e))));
-            cnt += (int)((j < NEc * K) & ahead);
+          uint64_t ke[S2];
+          uint32_t pe[S2];
+          int e[S2];
+          bool hv[S2];
+          int cnt[S2];
+#pragma unroll
+          for (int s = 0; s < S2; ++s) {
+            const int x = lane + 32 * s;
+            const int hs = x < NEc * K ? hsel[x / K] : -1;
+            hv[s] = hs >= 0;   // (always for x < NEc * K: C >= 32 lists, empty ones included)
+            const int cl = hv[s] ? hs : 0, q = x % K;
+            e[s] = cl * K + q;
+            ke[s] = hv[s] ? skey64(mb[cl].list[q].s) : 0ull;
+            pe[s] = hv[s] ? mb[cl].list[q].p : NO_INDEX;
+            cnt[s] = 0;
           }
-          if (hv && cnt < NEc) sorted[cnt] = e;
+#pragma unroll
+          for (int t = 0; t < S2; ++t) {
+#pragma unroll 8
+            for (int j = 0; j < 32; ++j) {
+              const uint64_t kf = __shfl_sync(0xffffffffu, ke[t], j);
+              const uint32_t pf = __shfl_sync(0xffffffffu, pe[t], j);
+              const int ef = __shfl_sync(0xffffffffu, e[t], j);
+              const bool in = j + 32 * t < NEc * K;
+#pragma unroll
+              for (int s = 0; s < S2; ++s) {
+                const bool ahead = (kf > ke[s]) | ((kf == ke[s]) & ((pf < pe[s]) | ((pf == pe[s]) & (ef < e[s]))));
+                cnt[s] += (int)(in & ahead);
+              }
+            }
+          }
+#pragma unroll
+          for (int s = 0; s < S2; ++s)
+            if (hv[s] && cnt[s] < NEc) sorted[cnt[s]] = e[s];
         }
         __syncthreads();
       }
@@ -1093,7 +1121,8 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
             vgeo<LGTW>(sp[u * W + v], sd[u], sd[v], k, j, rank, C, lgC, gg);
           }
           const int hp = (gg.Tr + TPI - 1) / TPI;   // items per row; its reciprocal for the items
-          gg.pad = hp > 1 ? (int)(0xFFFFFFFFu / (uint32_t)hp + 1u) : 0;
+          MPG_CHECK(hp < RCP_N, "items per row beyond the reciprocal table");
+          gg.pad = hp > 1 ? (int)rcp[hp] : 0;
           egeo[t] = gg;
           rect[t] = pack_rect(gg);
           const int rows = gg.nc > 0 ? gg.cntA + gg.cntB : 0;
@@ -1164,14 +1193,13 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
         const int bN = bu >= 0 ? sd[bu].N : 1;
         const int lb = lane < NEc ? lane : 0;
         for (int a = warp; a < NEc; a += NW) {  // warp: entry a, all target dictionaries
-          unsigned mm = 0u, cm = 0u;
-          for (int v = 0; v < W; ++v) {
-            const uint2 ra = rect[a * W + v], rb = rect[lb * W + v];
-            const bool meet = (lane < NEc) & rects_meet(ra, rb, sd[v].N);
-            const bool cover = (lane < NEc) & (bu == v) & rect_has(ra, bj, bt, bN);
-            mm |= __ballot_sync(0xffffffffu, meet);
-            cm |= __ballot_sync(0xffffffffu, cover);
-          }
+          bool meet = false;
+#pragma unroll 4
+          for (int v = 0; v < W; ++v) meet |= rects_meet(rect[a * W + v], rect[lb * W + v], sd[v].N);
+          // entry b's own tile lies in dictionary bu only
+          const bool cover = (lane < NEc) && bu >= 0 && rect_has(rect[a * W + (bu >= 0 ? bu : 0)], bj, bt, bN);
+          const unsigned mm = __ballot_sync(0xffffffffu, (lane < NEc) && meet);
+          const unsigned cm = __ballot_sync(0xffffffffu, cover);
           if (lane == 0) {
             wmeet[a] = mm;
             wcover[a] = cm;
@@ -1362,8 +1390,9 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
     // tile bookkeeping: record, candidate maximum, dirty level-0 node (stamp + list)
     const int stampv = round + 1;
     const uint64_t theta = TOPK == 2 ? cls->theta : 0ull;
-    auto finish = [&](int l, int g, R bs, uint32_t bp, R bre, R bim, auto upd) {
-      if (lane == warp_argmax_lane(bs, bp)) {
+    // (the winning lane of the tile's warp argmax)
+    auto finish_lane = [&](int l, int g, R bs, uint32_t bp, R bre, R bim, auto upd) {
+      {
         RecT rec;
         rec.s = bs;
         rec.re = bre;
@@ -1386,6 +1415,9 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
         const int node = l >> 5;
         if (!notree && atomicExch(&stamp[node], stampv) != stampv) list[atomicAdd(&cnt[0], 1)] = node;
       }
+    };
+    auto finish = [&](int l, int g, R bs, uint32_t bp, R bre, R bim, auto upd) {
+      if (lane == warp_argmax_lane(bs, bp)) finish_lane(l, g, bs, bp, bre, bim, upd);
     };
     // (g, v) of item gi: count the item bases <= gi (ibase is non-decreasing)
     auto item_gv = [&](int gi) {

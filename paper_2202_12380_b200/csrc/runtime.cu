@@ -265,6 +265,9 @@ extern "C" int mpgabor_kernels(mpgabor* h, double thr, void* stream) {
       pg.s_m = pg.M_c / dv.M;
       pg.s_n = std::max(1, dv.a / pg.a_c);
       pg.rstep = h->Rmax / pg.R;
+      pg.sh = (ilog2(pg.a_c) << PG_SH_AC) | (ilog2(pg.s_m) << PG_SH_SM) | (ilog2(pg.s_n) << PG_SH_SN) |
+              ((ilog2(pg.M_c) - ilog2(du.M)) << PG_SH_MCU) | ((ilog2(du.a) - ilog2(pg.a_c)) << PG_SH_AUC) |
+              (ilog2(dv.a) << PG_SH_AV);
       int lo, hi;
       h->nlag[i] = overlap_lags(du, dv, pg.a_c, lo, hi);
       h->nu_first[i] = lo;
@@ -468,6 +471,7 @@ static int plan_grids(mpgabor* h, int64_t L, int TW) {
     d.frame_off = (int32_t)foff;
     foff += d.N;
     d.MR = s.M / 2 + 1;
+    d.mr_magic = (uint32_t)((0x100000000ull + (uint64_t)d.MR - 1) / (uint64_t)d.MR);
     d.T = (d.MR + TW - 1) / TW;
     d.stride = d.T * TW;
     d.off = off;
