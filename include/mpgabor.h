@@ -252,21 +252,27 @@ int mpgabor_residual(mpgabor* h, double* out_dev, void* cuda_stream);
  * (one-selection kernel).  EINVAL outside [0, 3]. */
 int mpgabor_set_profile(mpgabor* h, int32_t mode);
 
-/* cycles (host int64[64]) of the last run with mode bit0, summed over the
+/* cycles (host int64[512]) of the last run with mode bit0, summed over the
  * iterations on CTA 0 / thread 0.  One-selection loop (mpgabor_set_batch 1):
  * [0] wait for the C roots (mailbox barrier), [1] selection + scalar step,
  * [2] block barrier after selection, [3] own update work, [4] block barrier
  * after the update, [5] level-1 refresh + barrier, [6] upper levels + root
  * publication; [7] iterations.  Multi-selection loop: [0] wait for the
- * messages, [1] verification, [2] barrier (window ranking on warps 1..),
- * [4] window geometry + scalar steps + barrier, [5] pair masks, [6] wait for the
- * pair warps, [29] walk set-up, [27] walk, [28] E chain + atoms, [9] item bases,
- * [10] barrier, [11] own items, [12] level refresh + barriers, [13] top-K,
- * [14] message push; [15] rounds; [16..19] own items: set-up, loads and update,
- * tile bookkeeping, items processed; [20] sum of the walk's last window position,
- * [21..26] walk end reasons (window, list exhausted, zero score, overlap, last list
- * entry); [30], [31] warp 1: wait, ranking; [40..55] CTAs 0..15: busy cycles
- * (messages received -> message published). */
+ * messages, [1] verification, [2] barrier (window ranking on warps 1..), [3]
+ * grid mode: stage-2 ranking, [4] window geometry + scalar steps + barrier, [5]
+ * pair masks, [6] wait for the pair warps, [29] walk set-up, [27] walk, [28] E
+ * chain + atoms, [9] item bases, [10] barrier, [11] own items, [12] barrier +
+ * level refresh, [13] top-K, [14] message push; [15] rounds; [16] candidate-list
+ * extraction, [17] candidate-list rebuilds (cycles), [19] rebuilds (count);
+ * [20] sum of the walk's last window position, [21..26] walk end reasons (batch
+ * full, window, list exhausted, zero score, overlap, last list entry); [30],
+ * [31] warp 1: wait, ranking; [40..55] CTAs 0..15: busy cycles (messages
+ * received -> message published); [56] roll-back rounds, [57..63] first rejected
+ * candidate 1..7; [64..191] CTAs 0..127: busy cycles; [192..319] CTAs 0..127:
+ * items; [320..447] CTAs 0..127: candidate-list rebuilds; [448..455] message
+ * waits of CTA 0 by length (< 1k, 1-2k, 2-3k, 3-4k, 4-6k, 6-8k, 8-12k, >= 12k
+ * cycles): counts, [456..463] their cycle sums; [464..467] rounds by the deepest
+ * CTA-list position (0..3) among the walk-window entries. */
 int mpgabor_last_profile(const mpgabor* h, int64_t* cycles);
 
 void mpgabor_destroy(mpgabor* h);

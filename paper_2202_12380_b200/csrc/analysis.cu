@@ -140,6 +140,117 @@ __global__ void __launch_bounds__(1024) dgt_kernel(const double* __restrict__ x,
   }
 }
 
+// The same analysis for M >= 32 with the register-blocked Stockham FFT (fft.cuh):
+// n/16 threads per frame, F frames per CTA, the frames in natural order at padded
+// shared-memory indices (no bit reversal, conflict-free radix-16 stores); the output
+// rows of the CTA's frames are contiguous in `out`, written by consecutive threads.
+template <typename R>
+__global__ void __launch_bounds__(512) dgt_stockham_kernel(const double* __restrict__ x, int64_t L, int a, int M, int gl,
+                                                           int N, const double* __restrict__ g,
+                                                           const double2* __restrict__ tw, int twres,
+                                                           typename cplx<R>::t* __restrict__ out, int stride, int F,
+                                                           uint32_t stride_magic, int write_pad) {
+  using C2 = typename cplx<R>::t;
+  extern __shared__ double2 z[];
+  const int n = M / 2;
+  const int lgn = 31 - __clz(n), lgM = lgn + 1;
+  const int lgtpf = lgn - 4;
+  const int j0 = -(gl / 2);
+  const int frame0 = blockIdx.x * F;
+  double* zd = reinterpret_cast<double*>(z);
+  // the post-processing twiddles W^m = e^{-2 pi i m/M}, m < n: consecutive m lie twstep
+  // table entries apart; for twstep >= 4 (scattered loads) they are staged in shared
+  // memory behind the frames, one table load per CTA instead of one per output
+  const int twstep = twres / (2 * n);
+  double2* wt = z + (F * n + ((F * n) >> 4));
+  const bool use_wt = twstep >= 4;
+  if (use_wt)
+    for (int m = threadIdx.x; m < n; m += blockDim.x) wt[m] = __ldg(&tw[(int64_t)m * twstep]);
+  // windowed frame folded modulo M, natural order: sample s -> value s >> 1, part s & 1
+  if (gl <= M) {  // one window sample per s: UF independent loads in flight per thread
+    constexpr int UF = 8;
+    const int total = F << lgM;
+    for (int i0 = threadIdx.x; i0 < total; i0 += UF * blockDim.x) {
+      double xv[UF], gv[UF];
+#pragma unroll
+      for (int u = 0; u < UF; ++u) {
+        const int idx = i0 + u * blockDim.x;
+        const int f = idx >> lgM, s = idx & (M - 1);
+        const int frame = frame0 + f;
+        const int j = j0 + ((s - j0) & (M - 1));
+        const bool ok = idx < total && frame < N && j < j0 + gl;
+        int64_t pos = (int64_t)frame * a + j;
+        pos += pos < 0 ? L : 0;
+        pos -= pos >= L ? L : 0;
+        xv[u] = ok ? __ldg(&x[pos]) : 0.0;
+        gv[u] = ok ? __ldg(&g[j - j0]) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < UF; ++u) {
+        const int idx = i0 + u * blockDim.x;
+        if (idx < total) zd[2 * pz(idx >> 1) + (idx & 1)] = xv[u] * gv[u];
+      }
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < F << lgM; idx += blockDim.x) {
+      const int f = idx >> lgM, s = idx & (M - 1);
+      const int frame = frame0 + f;
+      double v = 0.0;
+      if (frame < N) {
+        const int64_t base = (int64_t)frame * a;
+        for (int j = j0 + ((s - j0) & (M - 1)); j < j0 + gl; j += M) {
+          int64_t pos = base + j;
+          pos += pos < 0 ? L : 0;
+          pos -= pos >= L ? L : 0;
+          v += x[pos] * g[j - j0];
+        }
+      }
+      zd[2 * pz(idx >> 1) + (s & 1)] = v;
+    }
+  }
+  __syncthreads();
+  stockham_fft<-1>(z, lgn, lgtpf, tw, twres);
+  // X[m] = E[m] + W^m O[m] (fft.cuh rfft_bin), rows of the CTA's frames back to back
+  const int64_t o0 = (int64_t)frame0 * stride;
+  const int nval = min(F, N - frame0) * stride;
+  constexpr int UO = 4;   // outputs per thread per batch: their twiddle loads in flight together
+  for (int i0 = threadIdx.x; i0 < nval; i0 += UO * blockDim.x) {
+    double2 Wv[UO];
+    int mv[UO], fv[UO];
+#pragma unroll
+    for (int u = 0; u < UO; ++u) {
+      const int idx = i0 + u * blockDim.x;
+      const int f = (int)__umulhi((uint32_t)idx, stride_magic), m = idx - f * stride;
+      fv[u] = f;
+      mv[u] = idx < nval ? m : INT_MAX;
+      Wv[u] = (idx < nval && m < n) ? (use_wt ? wt[m] : __ldg(&tw[(int64_t)m * twstep])) : make_double2(-1.0, 0.0);  // W^n = -1
+    }
+#pragma unroll
+    for (int u = 0; u < UO; ++u) {
+      const int idx = i0 + u * blockDim.x, m = mv[u];
+      if (m == INT_MAX) continue;
+      C2 o;
+      if (m <= n) {
+        const int fb = fv[u] << lgn;
+        const double2 Zm = z[pz(fb + (m & (n - 1)))];
+        const double2 Zn = z[pz(fb + ((n - m) & (n - 1)))];
+        const double2 Zc = cconj(Zn);
+        const double2 E = make_double2(0.5 * (Zm.x + Zc.x), 0.5 * (Zm.y + Zc.y));
+        const double2 D = csub(Zm, Zc);
+        const double2 O = make_double2(0.5 * D.y, -0.5 * D.x);
+        const double2 X = cadd(E, cmul(Wv[u], O));
+        o.x = (R)X.x;
+        o.y = (R)X.y;
+      } else {
+        if (!write_pad) continue;
+        o.x = 0;
+        o.y = 0;
+      }
+      out[o0 + idx] = o;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // N2 kernel rows: for lag nu = nu_first + blockIdx.x
 //   b[s mod M_c] += g_u(s + nu a_c) g_v(s),  H[i][m] = sum_s b e^{-2 pi i m s/M_c}, m = 0..M_c/2
@@ -358,7 +469,25 @@ static int dgt_frames_per_cta(int M) { return max(1, 4096 / (M / 2)); }
 
 template <typename R>
 cudaError_t launch_dgt(const double* xp, int64_t L, const DictGeo& d, const double* g, const double2* tw,
-                       int twres, typename cplx<R>::t* out, cudaStream_t st) {
+                       int twres, typename cplx<R>::t* out, cudaStream_t st, int write_pad) {
+  if (d.M >= 32) {  // Stockham: n/16 threads per frame, >= 256 threads per CTA
+    const int tpf = d.M / 32;
+    int F = std::max(1, 256 / tpf);
+    while (F > 1 && (int64_t)F * d.stride >= (1 << 16)) F >>= 1;
+    if ((int64_t)F * d.stride >= (1 << 16)) return cudaErrorInvalidValue;
+    const int n = d.M / 2;
+    const bool use_wt = twres / d.M >= 4;   // (twstep = twres / (2n))
+    const size_t smem = (size_t)(F * n + (F * n) / 16 + (use_wt ? n : 0)) * sizeof(double2);
+    static bool attr_s = false;
+    if (!attr_s) {
+      CUDA_OK(cudaFuncSetAttribute(dgt_stockham_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      attr_s = true;
+    }
+    const uint32_t magic = (uint32_t)((0x100000000ull + (uint64_t)d.stride - 1) / (uint64_t)d.stride);
+    dgt_stockham_kernel<R><<<(d.N + F - 1) / F, F * tpf, smem, st>>>(xp, L, d.a, d.M, d.gl, d.N, g, tw, twres, out,
+                                                                      d.stride, F, magic, write_pad);
+    return cudaGetLastError();
+  }
   // (F * stride < 2^16 keeps the output row index by multiply-high exact)
   const int F = std::max(1, std::min(dgt_frames_per_cta(d.M), 65535 / d.stride));
   const size_t smem = (size_t)F * (d.M / 2) * sizeof(double2);
@@ -375,9 +504,9 @@ cudaError_t launch_dgt(const double* xp, int64_t L, const DictGeo& d, const doub
   return cudaGetLastError();
 }
 template cudaError_t launch_dgt<double>(const double*, int64_t, const DictGeo&, const double*, const double2*, int,
-                                        double2*, cudaStream_t);
+                                        double2*, cudaStream_t, int);
 template cudaError_t launch_dgt<float>(const double*, int64_t, const DictGeo&, const double*, const double2*, int,
-                                       float2*, cudaStream_t);
+                                       float2*, cudaStream_t, int);
 
 cudaError_t launch_kern_rows(int a_c, int M_c, int nu_first, int nlag, const double* gu, int glu, const double* gv,
                              int glv, const double2* tw, int twres, double2* H, cudaStream_t st) {

@@ -6,9 +6,11 @@ cudaError_t launch_window(int win, int gl, int a, int M, double* g, cudaStream_t
 cudaError_t launch_tables(double2* tw, int twres, double2* roots, int R, cudaStream_t st);
 cudaError_t launch_pad_energy(const double* x, int64_t Ls, double* xp, int64_t L, double* partial, int* nonfinite,
                               double* E0, cudaStream_t st);
+// write_pad = 0: leave the row padding (bins M/2+1 .. stride-1) alone -- it is zero from
+// an earlier analysis of the same layout and nothing else writes it
 template <typename R>
 cudaError_t launch_dgt(const double* xp, int64_t L, const DictGeo& d, const double* g, const double2* tw, int twres,
-                       typename cplx<R>::t* out, cudaStream_t st);
+                       typename cplx<R>::t* out, cudaStream_t st, int write_pad = 1);
 cudaError_t launch_kern_rows(int a_c, int M_c, int nu_first, int nlag, const double* gu, int glu, const double* gv,
                              int glv, const double2* tw, int twres, double2* H, cudaStream_t st);
 cudaError_t launch_kern_max_box(const double2* H, int nlag, int M_c, int nu_first, double thr, unsigned long long* mx,
@@ -47,7 +49,7 @@ struct LoopResult {
 constexpr int STOP_NONFINITE = -1;  // LoopResult.stop: x held NaN/Inf, the loop did not run
 
 constexpr int MAX_LEVELS = 6;
-constexpr int MPG_PROF_SLOTS = 320;  // mpgabor_last_profile slots
+constexpr int MPG_PROF_SLOTS = 512;  // mpgabor_last_profile slots
 constexpr int MAX_CLUSTER = 16;
 constexpr int TOP_SCAN = 256;   // the top node level (<= TOP_SCAN nodes) is scanned by one warp
 
@@ -94,6 +96,9 @@ struct LoopParams {
   int pedantic;                  // 1: select by the Eq. (20) energy (pedantic), else |c|^2
   int spec;                      // multi-selection: candidates per round (1..multi_max_batch())
   int topk_scan;                 // multi-selection: top-K by a scan of the tile records (no node tree upkeep)
+  int l2pf;                      // multi-selection: the first l2pf walk-window entries' grid rows and kernel
+                                 //   rows are bulk-prefetched into L2 after the window geometry (0: off;
+                                 //   set when the grid and kernels do not fit L2)
   void* backup;                  // multi-selection: per-CTA tile backups [C][bk_cap][TW] (cplx<R>)
   long long bk_cap;              // items per CTA per round the backup holds
   size_t smem_bytes;
@@ -113,6 +118,7 @@ int loop_max_cluster(bool f64, bool srec, int TW, int threads, size_t smem, bool
 constexpr int MULTI_K = MPG_MULTI_K;
 size_t multi_smem_bytes(const LoopParams& P, bool f64);
 int multi_max_batch();
+int multi_window();     // walk-window entries per round (NE)
 int multi_max_threads();  // the multi-selection kernel's launch bound (MPG_LB_THREADS)
 cudaError_t launch_multi_loop(const LoopParams& P, bool f64, int threads, cudaStream_t st);
 // gx: the global-exchange grid kernel; returns its co-resident CTA count

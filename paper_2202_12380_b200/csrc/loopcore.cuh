@@ -270,6 +270,15 @@ __device__ __forceinline__ void push_record(const Rec<R>& r, uint32_t raddr, uin
   for (int i = 0; i < (int)(sizeof(Rec<R>) / 16); ++i) st_async16(raddr + 16 * i, rbar, w[i]);
 }
 
+// Bulk prefetch of [p, p + bytes) into L2 by the TMA unit (cp.async.bulk.prefetch.L2,
+// fire and forget: no completion, no register or shared-memory destination); the range
+// is widened to 16-byte granules as the instruction requires.
+__device__ __forceinline__ void l2_prefetch_bulk(const void* p, uint32_t bytes) {
+  const unsigned long long a = (unsigned long long)p & ~15ull;
+  const uint32_t n = (uint32_t)(((unsigned long long)p + bytes - a + 15ull) & ~15ull);
+  if (bytes != 0) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(n) : "memory");
+}
+
 // one warp re-reduces node `node` of a level from its (up to) 32 children
 template <typename R>
 __device__ __forceinline__ void warp_node(const Rec<R>* child, long long nchild, int node, Rec<R>* out, int lane) {

@@ -299,7 +299,9 @@ __global__ void __launch_bounds__(512, 1) mp_loop_kernel(const LoopParams P) {
             const double X2 = tre * tre, Y2 = tim * tim, XY = tre * tim;
             Et = 2.0 * (X2 + Y2 + rre * (X2 - Y2) - 2.0 * rim * XY);
           }
-          const double En = Ecur - Et;
+          // (latency-floor mode: no update, so the energy is not reduced either -- the floor run
+          // does exactly the requested selections, whatever the atom energies)
+          const double En = P.floor_mode ? Ecur : Ecur - Et;
           if (lane == 0) {
             sel->tre = tre;
             sel->tim = tim;

@@ -17,6 +17,7 @@ size_t multi_smem_bytes(const LoopParams& P, bool f64) {
 }
 
 int multi_max_batch() { return BMAX; }
+int multi_window() { return NE; }
 int multi_max_threads() { return MPG_LB_THREADS; }
 
 cudaError_t launch_multi_loop(const LoopParams& P, bool f64, int threads, cudaStream_t st) {

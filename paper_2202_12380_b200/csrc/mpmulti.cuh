@@ -63,6 +63,12 @@ using namespace mpcore;
 #ifndef MPG_BMAX
 #define MPG_BMAX 8
 #endif
+#ifndef MPG_LB_THREADS
+#define MPG_LB_THREADS 512  // launch bound (max threads per CTA; 256 leaves 255 registers per thread)
+#endif
+#ifndef MPG_ECHAIN_BF
+#define MPG_ECHAIN_BF 1   // the round's energy chain without branches (0: the branching form)
+#endif
 constexpr int NE = MPG_NE;      // walk window: best merged list entries considered per round
 constexpr int BMAX = MPG_BMAX;  // candidates per round (upper bound; LoopParams::spec lowers it)
 static_assert(BMAX == 8 || BMAX == 16, "candidate slots: 8 or 16");
@@ -672,6 +678,28 @@ __device__ __forceinline__ unsigned long long gx_ld_acquire(const unsigned long 
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned long long gx_add_acq_rel(unsigned long long* p, unsigned long long v) {
+  unsigned long long o;
+  asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], %2;" : "=l"(o) : "l"(p), "l"(v) : "memory");
+  return o;
+}
+__device__ __forceinline__ void gx_st_relaxed(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// Grid-mode exchange protocol.  MPG_GX_COUNTER = 0 (default): every CTA releases its own
+// round stamp after its message; thread c of every CTA polls stamp c.  = 1: after writing
+// its message a CTA increments the round's arrival counter (acq_rel); the last arrival
+// resets it and releases one round flag, which a single thread per CTA polls (C pollers
+// of one line instead of C x C pollers of C stamps).  Measured slower (C4 5.29 vs 5.07
+// us/atom, C3 2.58 vs 2.56): the serialised increments cost more than the polling.
+// Counter and flag of parity ps at gx_stamp[32 + 16 ps] and gx_stamp[16 ps] (separate
+// 128-byte lines).  Correctness: the increments form a release sequence that the last
+// arrival's acq_rel read synchronises with, so every message happens-before the flag's
+// release; the reset happens-before the counter's next use two rounds later (every CTA
+// acquires the flag in between).
+#ifndef MPG_GX_COUNTER
+#define MPG_GX_COUNTER 0
+#endif
 
 // GX = false: one thread-block cluster of C <= 16 CTAs exchanging messages through
 // distributed shared memory (st.async + mbarrier).  GX = true: a cooperative grid of C
@@ -681,9 +709,6 @@ __device__ __forceinline__ unsigned long long gx_ld_acquire(const unsigned long 
 // identical.
 // TOPK: how a CTA finds its K best tiles each round -- 0 down the 32-ary node tree, 1 by a
 // scan of all its tile records, 2 from its candidate list (ClState).
-#ifndef MPG_LB_THREADS
-#define MPG_LB_THREADS 512  // launch bound (max threads per CTA; 256 leaves 255 registers per thread)
-#endif
 template <typename R, int TW, bool SREC, int K, bool GX, int TOPK = 0>
 __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopParams P) {
   using C2 = typename cplx<R>::t;
@@ -700,6 +725,7 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
   static_assert(TOPK != 1 || SREC, "the scan top-K reads shared-memory tile records");
   const int NEc = min(NE, C * K);
   const int B = max(1, min(BMAX, P.spec));
+  const bool floorm = P.floor_mode != 0;   // latency-floor measurement (no update)
 
   extern __shared__ __align__(32) unsigned char smem[];
   const Smem L = smem_layout(P, sizeof(RecT), sizeof(MsgT));
@@ -844,7 +870,15 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
         uint4* dstg = reinterpret_cast<uint4*>(reinterpret_cast<MsgT*>(P.gx_rec) + (long long)ps * C + rank);
 #pragma unroll
         for (int ch = 0; ch < (int)(sizeof(MsgT) / 16); ++ch) dstg[ch] = src[ch];
-        gx_st_release(P.gx_stamp + (long long)ps * C + rank, stamp);
+        if constexpr (MPG_GX_COUNTER) {
+          unsigned long long* cntp = P.gx_stamp + 32 + 16 * ps;
+          if (gx_add_acq_rel(cntp, 1ull) == (unsigned long long)(C - 1)) {
+            gx_st_relaxed(cntp, 0ull);
+            gx_st_release(P.gx_stamp + 16 * ps, stamp);
+          }
+        } else {
+          gx_st_release(P.gx_stamp + (long long)ps * C + rank, stamp);
+        }
       }
     } else {
       (void)stamp;
@@ -870,6 +904,8 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
       if (cls->need) {  // rebuild the list, extract again; a full scan if it cannot be exact
         const long long tr0 = prof ? clock64() : 0;
         if (prof) atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 19, 1ull);
+        if (P.prof != nullptr && slot == 0 && tid == 0 && rank < 128)   // rebuilds of every CTA
+          atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 320 + rank, 1ull);
         cl_rebuild<R, K>(hk, P.Lc, cls, clid, nmx, inl, lane, warp);
         if (prof) atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 17, (unsigned long long)(clock64() - tr0));
         if (warp == 0) {
@@ -906,9 +942,16 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
       // stamp, then copies its message into shared memory (L2 loads, L1 bypassed)
       const unsigned long long want = (unsigned long long)round + 1;
       constexpr int NCHUNK = (int)(sizeof(MsgT) / 16);
+      if constexpr (MPG_GX_COUNTER) {
+        if (tid == 0) {
+          const long long t0 = clock64();
+          while (gx_ld_acquire(P.gx_stamp + 16 * par) != want) spin_check(t0);
+        }
+        __syncthreads();
+      }
       for (int c = tid; c < C; c += blockDim.x) {
         const long long t0 = clock64();
-        while (gx_ld_acquire(P.gx_stamp + (long long)par * C + c) != want) {
+        while (!MPG_GX_COUNTER && gx_ld_acquire(P.gx_stamp + (long long)par * C + c) != want) {
           spin_check(t0);
         }
         const uint4* srcg = reinterpret_cast<const uint4*>(reinterpret_cast<const MsgT*>(P.gx_rec) + (long long)par * C + c);
@@ -925,6 +968,12 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
     if (warp == 0) {
       if constexpr (!GX) mbar_wait(smem_addr(&mbar[par]), (uint32_t)((round >> 1) & 1));
       if (P.prof != nullptr && slot == 0 && tid == 0) tbusy0 = clock64();
+      if (prof && round > 0) {  // histogram of the message waits (cycles; 8 buckets: <1k .. >=12k)
+        const long long w = clock64() - tprev;
+        const int bk = w < 1000 ? 0 : w < 2000 ? 1 : w < 3000 ? 2 : w < 4000 ? 3 : w < 6000 ? 4 : w < 8000 ? 5 : w < 12000 ? 6 : 7;
+        atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 448 + bk, 1ull);
+        atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 456 + bk, (unsigned long long)w);
+      }
       PROF_MARK(0);
       if (!GX && lane == 0) mbar_arm(smem_addr(&mbar[par]), C * msgbytes);  // slot reused at round + 2
 #ifdef MPG_CHECKS
@@ -1210,7 +1259,26 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
       __syncthreads();
       PROF_MARK(6);
       // ---- A4: the walk (warp 0, all lanes redundantly, bitmask logic); warps 1..
-      //      meanwhile compute every window entry's update geometry seen from this CTA
+      //      meanwhile (grids beyond L2, C3/C4) bulk-prefetch this CTA's rows of the first
+      //      l2pf window entries -- the hull tiles of every owned grid row and its kernel
+      //      row -- HBM -> L2 on the TMA unit, one (entry, dictionary) per warp, one row per
+      //      lane, so that the items of the picked entries hit L2
+      if (GX && warp != 0 && P.l2pf > 0) {   // (grid kernels only: the cluster's grids fit L2)
+        const int npf = min(P.l2pf, NEc) * W;
+        for (int t = warp - 1; t < npf; t += NW - 1) {
+          const VGeo& gg = egeo[t];
+          const int rows = gg.nc > 0 ? gg.cntA + gg.cntB : 0;
+          const DictGeo& dv = sd[t % W];
+          const C2* gb = grid + dv.grid_off + (long long)gg.t0 * TW;
+          for (int i = lane; i < rows; i += 32) {
+            const int rw2 = i < gg.cntA ? gg.rhoA + (i << lgC) : gg.rA + gg.rhoB + ((i - gg.cntA) << lgC);
+            int nrow = gg.n0 + rw2;
+            if (nrow >= dv.N) nrow -= dv.N;
+            l2_prefetch_bulk(gb + (long long)nrow * dv.stride, (uint32_t)(gg.Tr * TW * sizeof(C2)));
+            l2_prefetch_bulk(kern + gg.kbase + (long long)rw2 * gg.nc, (uint32_t)(gg.nc * sizeof(C2)));
+          }
+        }
+      }
       if (warp == 0) {
         const bool have = lane < NEc;
         const Ent& el = ent[have ? lane : 0];   // decoded in the geometry phase
@@ -1230,6 +1298,7 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
         PROF_MARK(29);
         unsigned excl = 0, picked = 0;
         int G = 0;
+        int pl = 0;                // lane g: window position of pick g (recorded as the walk takes it)
         int why = 0, lastpos = 0;  // walk statistics (profile mode)
         // the walk in window order, statically unrolled and branch-free (the state is
         // warp-uniform): entry j is skipped if a pick covers its tile; otherwise it
@@ -1255,6 +1324,7 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
           done = done | (cand & (w != 0));
           picked |= take ? bit : 0u;
           excl |= take ? cvr[j] : 0u;
+          pl = (take & (lane == G)) ? j : pl;
           G += take ? 1 : 0;
           lastpos = take ? j : lastpos;
           const bool e6 = take & ((lastm & bit) != 0u);  // its CTA list is consumed
@@ -1269,14 +1339,37 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
           atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 20, (unsigned long long)lastpos);
           atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 20 + why, 1ull);
         }
+        if (P.prof != nullptr && slot == 0 && rank == 0) {   // (warp-uniform: the whole warp reduces)
+          // deepest CTA-list position among the window entries (0..K-1, capped at 3)
+          const unsigned qd = __reduce_max_sync(0xffffffffu, have ? (unsigned)(sorted[lane] % K) : 0u);
+          if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 464 + min(qd, 3u), 1ull);
+        }
         // candidate g = the g-th picked window entry (lane g records its position);
         // E recurrence and the energy stop rules (Z15) in selection order, every lane
         // redundantly on the shuffled E~ of the picks
-        if ((picked >> lane) & 1u) st->pick[__popc(picked & ((1u << lane) - 1u))] = lane;
-        __syncwarp();
-        const int pl = lane < G ? st->pick[lane] : 0;
-        const double Etg = __shfl_sync(0xffffffffu, Etl, pl);
+        if (lane < G) st->pick[lane] = pl;
+        // (latency-floor mode: no update, so no energy change either -- E~ taken as 0)
+        const double Etg = floorm ? 0.0 : __shfl_sync(0xffffffffu, Etl, pl);
         const uint32_t kmine = __shfl_sync(0xffffffffu, keyl, pl);
+#if MPG_ECHAIN_BF
+        // E_{k+1} = E_k - E~ in selection order, branch-free: every lane runs the whole chain
+        // (the same rounded subtractions), lane g keeps the energy before (Epre) and after
+        // (Emine) pick g; the first pick whose Epre meets a stop rule (Z15) ends the round
+        const double E0r = st->E;
+        double Ecur = E0r, Emine = 0.0, Epre = 0.0;
+        double egs[BMAX];
+#pragma unroll
+        for (int g = 0; g < BMAX; ++g) egs[g] = __shfl_sync(0xffffffffu, Etg, g);
+#pragma unroll
+        for (int g = 0; g < BMAX; ++g) {
+          Epre = lane == g ? Ecur : Epre;
+          Ecur = Ecur - egs[g];
+          Emine = lane == g ? Ecur : Emine;
+        }
+        const unsigned fm = __ballot_sync(0xffffffffu, lane < G && (Epre <= Etols || Epre < 0.0));
+        int Gs = fm ? __ffs(fm) - 1 : G;
+        Ecur = Gs == 0 ? E0r : __shfl_sync(0xffffffffu, Emine, (Gs - 1) & 31);
+#else
         double Ecur = st->E, Emine = 0.0;
         int Gs = G;
 #pragma unroll
@@ -1291,6 +1384,7 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
             }
           }
         }
+#endif
         int stopr = 0;
         if (Gs == 0) {
           if (it0 >= P.maxit) stopr = 1;
@@ -1298,7 +1392,7 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
           else if (Ecur < 0.0) stopr = 3;
           else stopr = 4;
         }
-        if (P.floor_mode && Gs > 1) Gs = 1;
+        if (floorm && Gs > 1) Gs = 1;
         G = Gs;
         if (lane < G) {
           st->Enext[lane] = Emine;
@@ -1333,7 +1427,7 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
           const int t = lane * IPL + q;
           int nrw = 0, ntl = 0;
           const int v = t & 15;
-          if (t < GW && v < W && !P.floor_mode) {
+          if (t < GW && v < W && !floorm) {
             const int2 cn2 = ecnt[pq * 16 + v];
             nrw = cn2.x;
             ntl = cn2.y;

@@ -74,6 +74,11 @@ struct mpgabor {
   int cluster_req = 0, threads = 512, TW_req = 0, srec_req = 0;  // 0 = automatic
   int TW = 64, srec = 0;
   int run_threads = 512;  // threads of the planned loop launch
+  // grid slots [0, pad_clean) of the allocation pad_ptr hold zero row padding for the
+  // current layout: their analysis skips the padding stores (a new layout or a new
+  // allocation resets it)
+  int pad_clean = 0;
+  void* pad_ptr = nullptr;
   int batch = 0;          // candidates per round: 0 auto (multi-selection, multi_max_batch()), 1 one selection
   int kind = 2;           // loop kernel: 0 mploop.cu, 2 mpmulti.cu
   bool force_single = false;  // multi-selection impossible for this layout: use mploop.cu
@@ -458,6 +463,7 @@ extern "C" int mpgabor_set_launch(mpgabor* h, int32_t cluster, int32_t threads, 
 // grids and tiles of every dictionary for tile width TW (fills h->geo, sizes)
 static int plan_grids(mpgabor* h, int64_t L, int TW) {
   const int W = h->W;
+  h->pad_clean = 0;
   h->geo.assign(W, DictGeo{});
   int64_t off = 0, goff = 0, toff = 0, foff = 0;
   for (int w = 0; w < W; ++w) {
@@ -679,6 +685,19 @@ static int ensure_layout(mpgabor* h, int64_t Ls) {
       }
     }
   }
+  // multi-selection over residual grids and kernels larger than L2 (C4: 1.07 GB + 0.36 GB):
+  // bulk-prefetch the walk window's rows into L2 (mpmulti.cu, after the window geometry);
+  // env MPGABOR_L2PF = number of window entries overrides, for measurements
+  {
+    int dev = 0, l2 = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev) != cudaSuccess) {
+      cudaGetLastError();
+      l2 = 0;
+    }
+    const double bytes = (double)h->celem() * ((double)h->grid_elems + (double)h->kern_elems);
+    const char* ev = std::getenv("MPGABOR_L2PF");
+    P.l2pf = h->kind == 2 ? (ev ? std::max(0, std::atoi(ev)) : (l2 > 0 && bytes > (double)l2 ? multi_window() : 0)) : 0;
+  }
   h->lay_C = P.C;
   // buffers
   TRY_CUDA(h, h->d_geo.ensure(sizeof(DictGeo) * W));
@@ -696,7 +715,7 @@ static int ensure_layout(mpgabor* h, int64_t Ls) {
     // one-selection kernel: [2][C] root records; multi-selection kernel: [2][C] messages
     TRY_CUDA(h, h->gxrec.ensure(std::max(h->f64() ? sizeof(Rec<double>) : sizeof(Rec<float>), multi_msg_bytes(h->f64())) *
                                 2 * P.C));
-    TRY_CUDA(h, h->gxstamp.ensure(sizeof(unsigned long long) * 2 * P.C));
+    TRY_CUDA(h, h->gxstamp.ensure(sizeof(unsigned long long) * std::max(2 * P.C, 64)));  // (>= 64: mpmulti.cuh GX_COUNTER)
   }
   if (h->kind == 2) {
     // roll-back backups: per CTA and round at most spec x max_u sum_v (rows/C + 1) x (hull tiles)
@@ -785,7 +804,12 @@ static int run_impl(mpgabor* h, const double* x_dev, int64_t Ls, int64_t maxit, 
   const size_t recsz = h->f64() ? sizeof(Rec<double>) : sizeof(Rec<float>);
   TRY_CUDA(h, cudaEventRecord(h->ev[0], st));
   TRY_CUDA(h, cudaMemsetAsync(h->flag.p, 0, sizeof(int), st));
+  if (h->grid.p != h->pad_ptr) {
+    h->pad_ptr = h->grid.p;
+    h->pad_clean = 0;
+  }
   for (int b = 0; b < B; ++b) {
+    const int write_pad = b >= h->pad_clean ? 1 : 0;
     TRY_LAUNCH(h, 2, launch_pad_energy(x_dev + (int64_t)b * Ls, Ls, h->xp.as<double>(), h->L, h->partial.as<double>(),
                                        h->flag.as<int>(), h->E0.as<double>() + b, st));
     for (int w = 0; w < W; ++w) {
@@ -794,12 +818,13 @@ static int run_impl(mpgabor* h, const double* x_dev, int64_t Ls, int64_t maxit, 
       const int64_t goff = d.grid_off + (int64_t)b * h->grid_elems;
       if (h->f64())
         TRY_LAUNCH(h, 1, launch_dgt<double>(h->xp.as<double>(), h->L, d, g, h->tw.as<double2>(), h->twres,
-                                            h->grid.as<double2>() + goff, st));
+                                            h->grid.as<double2>() + goff, st, write_pad));
       else
         TRY_LAUNCH(h, 1, launch_dgt<float>(h->xp.as<double>(), h->L, d, g, h->tw.as<double2>(), h->twres,
-                                           h->grid.as<float2>() + goff, st));
+                                           h->grid.as<float2>() + goff, st, write_pad));
     }
   }
+  h->pad_clean = std::max(h->pad_clean, B);
   TRY_CUDA(h, cudaEventRecord(h->ev[1], st));
   const SelScore sel{h->pedantic, h->rho.as<RhoEnt>(), h->rho_meta.as<int>()};
   for (int b = 0; b < B; ++b) {
@@ -866,7 +891,7 @@ static int run_impl(mpgabor* h, const double* x_dev, int64_t Ls, int64_t maxit, 
   P.gx_rec = nullptr;
   P.gx_stamp = nullptr;
   if (h->gx) {  // stamps start at 0: the first roots carry stamp 1
-    TRY_CUDA(h, cudaMemsetAsync(h->gxstamp.p, 0, sizeof(unsigned long long) * 2 * P.C, st));
+    TRY_CUDA(h, cudaMemsetAsync(h->gxstamp.p, 0, sizeof(unsigned long long) * std::max(2 * P.C, 64), st));
     P.gx_rec = h->gxrec.p;
     P.gx_stamp = h->gxstamp.as<unsigned long long>();
   }

@@ -253,7 +253,7 @@ def mpgabor_set_profile(h, mode):
 
 
 def mpgabor_last_profile(h):
-    c = (_I64 * 320)()
+    c = (_I64 * 512)()
     _check(h, _lib.mpgabor_last_profile(h, c))
     return list(c)
 

@@ -134,6 +134,29 @@ def test_dgt_matches_oracle(mpg, name, prec):
     mp.close()
 
 
+# every channel count M the library takes (Z25) through both DGT kernels: the radix-2
+# kernel (M < 32) and the register-blocked Stockham FFT (M >= 32: radix-2/4/8 first pass,
+# then radix-16 passes), redundancies 4 and 8, a window shorter than M and one longer
+DGT_DICTS = ([Dict(BLACKMAN, M, max(1, M // 4), M) for M in (2, 4, 8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096,
+                                                              8192, 16384)]
+             + [Dict(BLACKMAN, M, M // 8, M) for M in (32, 256, 2048, 16384)]
+             + [Dict(HANN, M // 2, M // 4, M) for M in (64, 1024)]
+             + [Dict(GAUSS, 97, 16, 64)])
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("d", DGT_DICTS, ids=lambda d: f"w{d.win}gl{d.gl}a{d.a}M{d.M}")
+def test_dgt_every_channel_count(mpg, d, prec):
+    x = random_signal(65536 - 77, 5)      # ragged: zero-padded to a multiple of lcm(a, M)
+    S = oracle.Setup.build(x, (d,), 1e-4)
+    mp, out, _ = gpu_run(mpg, (d,), 1e-4, x, 0, -math.inf, prec)
+    res = mp.residual(x.size).cpu().numpy()
+    ref = S.grids[0].ravel()
+    tol = 1e-12 if prec == "f64" else 1e-6
+    assert np.max(np.abs(res - ref)) <= tol * math.sqrt(S.E0)
+    mp.close()
+
+
 # ---------------------------------------------------------------------------
 # full runs
 # ---------------------------------------------------------------------------

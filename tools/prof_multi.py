@@ -48,5 +48,15 @@ for name in cfgs:
               f"min {min(items):.2f} max {max(items):.2f}", flush=True)
         print(f"   candidate-list rebuilds: {c[19]} ({100 * c[19] / n:.2f} % of rounds), "
               f"{c[17] / max(c[19], 1):.0f} cycles each; extraction {c[16] / n:.0f} cycles/round", flush=True)
+        rb = [c[320 + r] for r in range(Cn)]
+        print(f"   rebuilds over {Cn} CTAs: total {sum(rb)} ({100 * sum(rb) / n:.1f} % of rounds if disjoint), "
+              f"min {min(rb)} max {max(rb)}", flush=True)
+        labels = ["<1k", "1-2k", "2-3k", "3-4k", "4-6k", "6-8k", "8-12k", ">=12k"]
+        print("   CTA 0 message waits: " + " ".join(
+            f"{labels[i]}: {c[448 + i]} ({c[456 + i] / max(c[448 + i], 1):.0f})" for i in range(8))
+              + f"; share of wait cycles in rounds waiting >= 4k: "
+              f"{sum(c[460:464]) / max(sum(c[456:464]), 1):.2f}", flush=True)
+        print("   deepest CTA-list position in the walk window (0..3): "
+              + " ".join(str(c[464 + i]) for i in range(4)), flush=True)
         mp.set_profile(0)
     mp.close()
