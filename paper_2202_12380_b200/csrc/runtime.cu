@@ -685,7 +685,7 @@ static int ensure_layout(mpgabor* h, int64_t Ls) {
       }
     }
   }
-  // multi-selection over residual grids and kernels larger than L2 (C4: 1.07 GB + 0.36 GB):
+  // multi-selection over residual grids and kernels much larger than L2 (C4: 1.07 GB + 0.36 GB):
   // bulk-prefetch the walk window's rows into L2 (mpmulti.cu, after the window geometry);
   // env MPGABOR_L2PF = number of window entries overrides, for measurements
   {
@@ -696,7 +696,8 @@ static int ensure_layout(mpgabor* h, int64_t Ls) {
     }
     const double bytes = (double)h->celem() * ((double)h->grid_elems + (double)h->kern_elems);
     const char* ev = std::getenv("MPGABOR_L2PF");
-    P.l2pf = h->kind == 2 ? (ev ? std::max(0, std::atoi(ev)) : (l2 > 0 && bytes > (double)l2 ? multi_window() : 0)) : 0;
+    // (on when they exceed 4x L2: C4 5.13 -> 5.08 us/atom; C3, 2.3x L2, 2.558 -> 2.577 with it)
+    P.l2pf = h->kind == 2 ? (ev ? std::max(0, std::atoi(ev)) : (l2 > 0 && bytes > 4.0 * (double)l2 ? multi_window() : 0)) : 0;
   }
   h->lay_C = P.C;
   // buffers
