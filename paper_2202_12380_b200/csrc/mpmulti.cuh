@@ -148,9 +148,13 @@ struct ClState {
   int above;                     // radix select: entries above the current range
   int done;                      // radix select finished
   int valid;                     // 0: the rebuild could not make an exact list (ties) -> scan
-  int need;                      // 1: rebuild before the next extraction
-  int pad_;
+  int need;                      // 1: the list could not give the exact top K (scan), rebuild it
+  int soon;                      // 1: fewer than CL_LOW entries left -- rebuild after this publication
 };
+#ifndef MPG_CL_LOW
+#define MPG_CL_LOW 8
+#endif
+constexpr int CL_LOW = MPG_CL_LOW;   // list length below which the list is rebuilt pre-emptively
 
 __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 // items per row hp = ceil(hull tiles / tiles per item) <= ceil(257 / 2) (M <= 16384, TW >= 32)
@@ -618,7 +622,10 @@ __device__ __forceinline__ bool cl_extract_nc(const Rec<R>* trec, ClState* cs, i
     base += __popc(km);
   }
   __syncwarp();
-  if (lane == 0) cs->n = base;
+  if (lane == 0) {
+    cs->n = base;
+    cs->soon = base < CL_LOW ? 1 : 0;
+  }
   warp_topk_nc<K, NC>(kk, pk, ik, tk, lane);
   __syncwarp();
   return n <= CL_CAP && (base >= K || th == 1ull);
@@ -901,24 +908,35 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
       }
       if (prof) atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 16, (unsigned long long)(clock64() - tx0));
       __syncthreads();
-      if (cls->need) {  // rebuild the list, extract again; a full scan if it cannot be exact
+      // the list cannot give the exact top K: a full scan this round; the list is rebuilt
+      // after the publication (rebuild_after), off the path to the message
+      if (cls->need) cta_topk_scan<R, K>(trec, P.Lc, tk, wk, lane, warp, NW);
+    } else if constexpr (TOPK == 1) {
+      cta_topk_scan<R, K>(trec, P.Lc, tk, wk, lane, warp, NW);
+    } else {
+      cta_topk<R, K>(P, lev, trec, tk, lane, warp, NW);
+    }
+  };
+  // candidate lists: rebuild after the message is out (all threads) when the extraction ran
+  // short (need) or left fewer than CL_LOW entries (soon).  A CTA waits for its peers'
+  // messages at this point anyway, so the rebuild is hidden unless this CTA is the
+  // round's last; before, a rebuild before the publication stalled every peer that round.
+  // The list invariant holds across it: the next items add every rewritten tile >= theta.
+  auto rebuild_after = [&]() {
+    if constexpr (TOPK == 2) {
+      if (cls->need | cls->soon) {   // (uniform: both written before the top-K barrier)
         const long long tr0 = prof ? clock64() : 0;
         if (prof) atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 19, 1ull);
         if (P.prof != nullptr && slot == 0 && tid == 0 && rank < 128)   // rebuilds of every CTA
           atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 320 + rank, 1ull);
         cl_rebuild<R, K>(hk, P.Lc, cls, clid, nmx, inl, lane, warp);
         if (prof) atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 17, (unsigned long long)(clock64() - tr0));
-        if (warp == 0) {
-          const bool ok = cls->valid && cl_extract<R, K>(trec, cls, clid, inl, tk, lane);
-          if (lane == 0) cls->need = ok ? 0 : 1;
+        if (tid == 0) {
+          cls->need = 0;
+          cls->soon = 0;
         }
         __syncthreads();
-        if (cls->need) cta_topk_scan<R, K>(trec, P.Lc, tk, wk, lane, warp, NW);
       }
-    } else if constexpr (TOPK == 1) {
-      cta_topk_scan<R, K>(trec, P.Lc, tk, wk, lane, warp, NW);
-    } else {
-      cta_topk<R, K>(P, lev, trec, tk, lane, warp, NW);
     }
   };
   if constexpr (TOPK == 2) {
@@ -931,6 +949,7 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
   }
   topk();
   if (warp == 0) publish(0, 1ull);
+  rebuild_after();
 
   long long rounds = 0;
   long long tbusy0 = 0;
@@ -1732,6 +1751,7 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
       }
     }
     if (warp == 0) publish(par ^ 1, (unsigned long long)round + 2);
+    rebuild_after();
   }
   if (rank == 0 && tid == 0) {
     P.result[slot].n_done = st->it;
