@@ -272,7 +272,9 @@ int mpgabor_set_profile(mpgabor* h, int32_t mode);
  * items; [320..447] CTAs 0..127: candidate-list rebuilds; [448..455] message
  * waits of CTA 0 by length (< 1k, 1-2k, 2-3k, 3-4k, 4-6k, 6-8k, 8-12k, >= 12k
  * cycles): counts, [456..463] their cycle sums; [464..467] rounds by the deepest
- * CTA-list position (0..3) among the walk-window entries. */
+ * CTA-list position (0..3) among the walk-window entries; [468..472] candidate-list
+ * rebuilds of CTA 0: node maxima, rank counts, gathers (cycles), rank-halving retries,
+ * rebuilds. */
 int mpgabor_last_profile(const mpgabor* h, int64_t* cycles);
 
 void mpgabor_destroy(mpgabor* h);

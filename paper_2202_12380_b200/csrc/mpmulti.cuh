@@ -519,9 +519,20 @@ __device__ __forceinline__ uint32_t hkey(R s) {
 // caller extracts by a full scan until a later rebuild succeeds.
 template <typename R, int K>
 __device__ __noinline__ void cl_rebuild(const uint32_t* hk, long long Lc, ClState* cs, int* clid, uint32_t* nm,
-                                        unsigned char* inl, int lane, int warp) {
+                                        unsigned char* inl, int lane, int warp, unsigned long long* pf) {
   const int tid = threadIdx.x, nthr = blockDim.x, NW = nthr >> 5;
   const int nn = (int)((Lc + 31) >> 5);
+  // profile (pf != null on thread 0 of CTA 0): [0] node maxima, [1] rank counts, [2] gathers,
+  // [3] rank-halving retries, [4] calls -- cycles summed over the rebuilds
+  long long tp = pf ? clock64() : 0;
+  auto mark = [&](int i) {
+    if (pf) {
+      const long long tn = clock64();
+      atomicAdd(pf + i, (unsigned long long)(tn - tp));
+      tp = tn;
+    }
+  };
+  if (pf) atomicAdd(pf + 4, 1ull);
   {  // the old list's membership flags (inl[l] = 1 exactly for the stored entries)
     const int n0 = min(cs->n, CL_CAP);
     for (int i = tid; i < n0; i += nthr) inl[clid[i]] = 0;
@@ -532,6 +543,7 @@ __device__ __noinline__ void cl_rebuild(const uint32_t* hk, long long Lc, ClStat
     if (lane == 0) nm[q] = m;
   }
   __syncthreads();
+  mark(0);
   for (int T = CL_TARGET;; T >>= 1) {
     if (tid == 0) {
       cs->n = 0;
@@ -539,16 +551,32 @@ __device__ __noinline__ void cl_rebuild(const uint32_t* hk, long long Lc, ClStat
       cs->valid = 1;
     }
     __syncthreads();
-    for (int t = tid; t < nn; t += nthr) {
-      const uint32_t v = nm[t];
-      int r = 0;
-      for (int j = 0; j < nn; ++j) {
-        const uint32_t u = nm[j];
-        r += (u > v) | ((u == v) & (j < t));
+    // rank of node t (value desc, index asc): two threads per node (adjacent lanes), each
+    // over half of the nodes with four independent partial counts (loads in flight)
+    for (int t2 = tid; t2 < 2 * ((nn + 15) & ~15); t2 += nthr) {
+      const int t = t2 >> 1, h = t2 & 1;
+      const uint32_t v = t < nn ? nm[t] : 0u;
+      const int half = (nn + 1) >> 1;
+      const int j0 = h * half, j1 = min(nn, j0 + half);
+      int r0 = 0, r1 = 0, r2 = 0, r3 = 0;
+      int j = j0;
+      for (; j + 3 < j1; j += 4) {
+        const uint32_t u0 = nm[j], u1 = nm[j + 1], u2 = nm[j + 2], u3 = nm[j + 3];
+        r0 += (u0 > v) | ((u0 == v) & (j < t));
+        r1 += (u1 > v) | ((u1 == v) & (j + 1 < t));
+        r2 += (u2 > v) | ((u2 == v) & (j + 2 < t));
+        r3 += (u3 > v) | ((u3 == v) & (j + 3 < t));
       }
-      if (r == T - 1 && v != 0u) cs->theta = (uint64_t)v << 32;
+      for (; j < j1; ++j) {
+        const uint32_t u = nm[j];
+        r0 += (u > v) | ((u == v) & (j < t));
+      }
+      int r = r0 + r1 + r2 + r3;
+      r += __shfl_xor_sync(0xffffffffu, r, 1);
+      if (h == 0 && t < nn && r == T - 1 && v != 0u) cs->theta = (uint64_t)v << 32;
     }
     __syncthreads();
+    mark(1);
     const uint64_t th = cs->theta;
     const uint32_t thw = th == 1ull ? 1u : (uint32_t)(th >> 32);
     for (int q = warp; q < nn; q += NW) {
@@ -566,8 +594,10 @@ __device__ __noinline__ void cl_rebuild(const uint32_t* hk, long long Lc, ClStat
       }
     }
     __syncthreads();
+    mark(2);
     const int n = cs->n;
     if (n <= CL_CAP) break;
+    if (pf) atomicAdd(pf + 3, 1ull);
     // overflow: unmark, retry with half the rank target (T = 1 cannot shrink further)
     for (int i = tid; i < CL_CAP; i += nthr) inl[clid[i]] = 0;
     if (T == 1) {
@@ -929,7 +959,8 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
         if (prof) atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 19, 1ull);
         if (P.prof != nullptr && slot == 0 && tid == 0 && rank < 128)   // rebuilds of every CTA
           atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 320 + rank, 1ull);
-        cl_rebuild<R, K>(hk, P.Lc, cls, clid, nmx, inl, lane, warp);
+        cl_rebuild<R, K>(hk, P.Lc, cls, clid, nmx, inl, lane, warp,
+                         prof ? reinterpret_cast<unsigned long long*>(P.prof) + 468 : nullptr);
         if (prof) atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 17, (unsigned long long)(clock64() - tr0));
         if (tid == 0) {
           cls->need = 0;
