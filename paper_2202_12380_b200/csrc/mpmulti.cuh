@@ -155,6 +155,8 @@ struct ClState {
 #define MPG_CL_LOW 8
 #endif
 constexpr int CL_LOW = MPG_CL_LOW;   // list length below which the list is rebuilt pre-emptively
+constexpr int CL_NBK = 256;          // rebuild: buckets of node maxima below the largest
+constexpr int CL_BSH = 16;           //   of 2^16 in the upper score word each (1/16 octave of the score)
 
 __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 // items per row hp = ceil(hull tiles / tiles per item) <= ceil(257 / 2) (M <= 16384, TW >= 32)
@@ -241,8 +243,8 @@ __host__ __device__ inline Smem smem_layout(const LoopParams& P, size_t recsz, s
   o += sizeof(uint32_t) * RCP_N;
   s.hk = o;                   // candidate lists: upper 32 bits of every tile's score key
   o += P.topk_scan == 2 ? sizeof(uint32_t) * (size_t)P.Lc : 0;
-  s.nmax = o;                 // candidate lists: node maxima of hk (rebuilds)
-  o += P.topk_scan == 2 ? sizeof(uint32_t) * (size_t)((P.Lc + 31) / 32) : 0;
+  s.nmax = o;                 // candidate lists: node maxima of hk and their bucket counts (rebuilds)
+  o += P.topk_scan == 2 ? sizeof(uint32_t) * (size_t)((P.Lc + 31) / 32 + CL_NBK + 1) : 0;
   s.total = align_up(o, 16);
   return s;
 }
@@ -509,8 +511,10 @@ __device__ __forceinline__ uint32_t hkey(R s) {
 // current by the items):
 //   1. node maxima nm[q] = max of the words of tiles 32q .. 32q+31 (one warp reduction
 //      per node);
-//   2. thw = the node maximum of rank T-1 (rank counting over the nodes, ties by node
-//      index), or every positive word when there are fewer than T positive nodes;
+//   2. thw = the lower edge of the first bucket of node maxima (1/16 octave each below the
+//      largest, one shared atomic per node) at which the node count reaches T -- at least
+//      T nodes, hence tiles, lie at or above it -- or every positive word when fewer than T
+//      nodes lie within 16 octaves (a rank count over the nodes took 3.2k-9.3k cycles);
 //   3. the list = every tile whose word is >= thw, gathered from the nodes whose maximum
 //      reaches thw (one ballot per node).  At least T tiles qualify; if more than
 //      CL_CAP do, T is halved and the list gathered again.
@@ -519,10 +523,11 @@ __device__ __forceinline__ uint32_t hkey(R s) {
 // caller extracts by a full scan until a later rebuild succeeds.
 template <typename R, int K>
 __device__ __noinline__ void cl_rebuild(const uint32_t* hk, long long Lc, ClState* cs, int* clid, uint32_t* nm,
-                                        unsigned char* inl, int lane, int warp, unsigned long long* pf) {
+                                        unsigned char* inl, int lane, int warp, unsigned long long* pf,
+                                        bool hist_first) {
   const int tid = threadIdx.x, nthr = blockDim.x, NW = nthr >> 5;
   const int nn = (int)((Lc + 31) >> 5);
-  // profile (pf != null on thread 0 of CTA 0): [0] node maxima, [1] rank counts, [2] gathers,
+  // profile (pf != null on thread 0 of CTA 0): [0] node maxima, [1] thresholds, [2] gathers,
   // [3] rank-halving retries, [4] calls -- cycles summed over the rebuilds
   long long tp = pf ? clock64() : 0;
   auto mark = [&](int i) {
@@ -533,47 +538,101 @@ __device__ __noinline__ void cl_rebuild(const uint32_t* hk, long long Lc, ClStat
     }
   };
   if (pf) atomicAdd(pf + 4, 1ull);
+  uint32_t* hist = nm + nn;   // [CL_NBK] node counts per bucket, [CL_NBK] = the largest node maximum
   {  // the old list's membership flags (inl[l] = 1 exactly for the stored entries)
     const int n0 = min(cs->n, CL_CAP);
     for (int i = tid; i < n0; i += nthr) inl[clid[i]] = 0;
   }
-  for (int q = warp; q < nn; q += NW) {
-    const long long i = (long long)q * 32 + lane;
-    const uint32_t m = __reduce_max_sync(0xffffffffu, i < Lc ? hk[i] : 0u);
-    if (lane == 0) nm[q] = m;
+  for (int b = tid; b <= CL_NBK; b += nthr) hist[b] = 0u;
+  __syncthreads();
+  {
+    uint32_t wm = 0u;
+    for (int q = warp; q < nn; q += NW) {
+      const long long i = (long long)q * 32 + lane;
+      const uint32_t m = __reduce_max_sync(0xffffffffu, i < Lc ? hk[i] : 0u);
+      if (lane == 0) nm[q] = m;
+      wm = max(wm, m);
+    }
+    if (lane == 0 && wm != 0u) atomicMax(&hist[CL_NBK], wm);
   }
   __syncthreads();
   mark(0);
-  for (int T = CL_TARGET;; T >>= 1) {
-    if (tid == 0) {
-      cs->n = 0;
-      cs->theta = 1ull;   // (no node of rank T-1 with a positive maximum: every positive word)
-      cs->valid = 1;
+  // node maxima by bucket below the largest: (mx - m) >> CL_BSH, the last bucket holding
+  // everything further down (one shared atomic per node)
+  const uint32_t mx = hist[CL_NBK];
+  if (hist_first) {
+    for (int q = tid; q < nn; q += nthr) {
+      const uint32_t m = nm[q];
+      if (m != 0u) atomicAdd(&hist[min((mx - m) >> CL_BSH, (uint32_t)(CL_NBK - 1))], 1u);
     }
     __syncthreads();
-    // rank of node t (value desc, index asc): two threads per node (adjacent lanes), each
-    // over half of the nodes with four independent partial counts (loads in flight)
-    for (int t2 = tid; t2 < 2 * ((nn + 15) & ~15); t2 += nthr) {
-      const int t = t2 >> 1, h = t2 & 1;
-      const uint32_t v = t < nn ? nm[t] : 0u;
-      const int half = (nn + 1) >> 1;
-      const int j0 = h * half, j1 = min(nn, j0 + half);
-      int r0 = 0, r1 = 0, r2 = 0, r3 = 0;
-      int j = j0;
-      for (; j + 3 < j1; j += 4) {
-        const uint32_t u0 = nm[j], u1 = nm[j + 1], u2 = nm[j + 2], u3 = nm[j + 3];
-        r0 += (u0 > v) | ((u0 == v) & (j < t));
-        r1 += (u1 > v) | ((u1 == v) & (j + 1 < t));
-        r2 += (u2 > v) | ((u2 == v) & (j + 2 < t));
-        r3 += (u3 > v) | ((u3 == v) & (j + 3 < t));
+  }
+  for (int T = CL_TARGET;; T >>= 1) {
+    if (T < CL_TARGET || !hist_first) {
+      // the exact node maximum of rank T-1, by a rank count over the nodes (two threads per
+      // node, ties by node index): after an overflow (crowded bucket), and for the grid
+      // kernels (C4: its late rounds' crowded buckets overflow often, 5.03 -> 5.08 us/atom)
+      if (tid == 0) {
+        cs->n = 0;
+        cs->theta = 1ull;   // (no node of rank T-1 with a positive maximum: every positive word)
+        cs->valid = 1;
       }
-      for (; j < j1; ++j) {
-        const uint32_t u = nm[j];
-        r0 += (u > v) | ((u == v) & (j < t));
+      __syncthreads();
+      for (int t2 = tid; t2 < 2 * ((nn + 15) & ~15); t2 += nthr) {
+        const int t = t2 >> 1, h = t2 & 1;
+        const uint32_t v = t < nn ? nm[t] : 0u;
+        const int half = (nn + 1) >> 1;
+        const int j0 = h * half, j1 = min(nn, j0 + half);
+        int r0 = 0, r1 = 0, r2 = 0, r3 = 0;
+        int j = j0;
+        for (; j + 3 < j1; j += 4) {
+          const uint32_t u0 = nm[j], u1 = nm[j + 1], u2 = nm[j + 2], u3 = nm[j + 3];
+          r0 += (u0 > v) | ((u0 == v) & (j < t));
+          r1 += (u1 > v) | ((u1 == v) & (j + 1 < t));
+          r2 += (u2 > v) | ((u2 == v) & (j + 2 < t));
+          r3 += (u3 > v) | ((u3 == v) & (j + 3 < t));
+        }
+        for (; j < j1; ++j) {
+          const uint32_t u = nm[j];
+          r0 += (u > v) | ((u == v) & (j < t));
+        }
+        int r = r0 + r1 + r2 + r3;
+        r += __shfl_xor_sync(0xffffffffu, r, 1);
+        if (h == 0 && t < nn && r == T - 1 && v != 0u) cs->theta = (uint64_t)v << 32;
       }
-      int r = r0 + r1 + r2 + r3;
-      r += __shfl_xor_sync(0xffffffffu, r, 1);
-      if (h == 0 && t < nn && r == T - 1 && v != 0u) cs->theta = (uint64_t)v << 32;
+    } else if (warp == 0) {
+      // the first bucket (below the last) at which the node count reaches T: its lower edge
+      // thw has at least T nodes -- hence tiles -- at or above it; none: every positive word
+      constexpr int PL = CL_NBK / 32;
+      uint32_t c[PL], sum = 0u;
+#pragma unroll
+      for (int k = 0; k < PL; ++k) {
+        const int b = lane * PL + k;
+        c[k] = b < CL_NBK - 1 ? hist[b] : 0u;
+        sum += c[k];
+      }
+      uint32_t incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      uint32_t run = incl - sum;
+      int bsel = -1;
+#pragma unroll
+      for (int k = 0; k < PL; ++k) {
+        run += c[k];
+        if (bsel < 0 && run >= (uint32_t)T) bsel = lane * PL + k;
+      }
+      const unsigned has = __ballot_sync(0xffffffffu, bsel >= 0);
+      const int b = has ? __shfl_sync(0xffffffffu, bsel, __ffs(has) - 1) : -1;
+      if (lane == 0) {
+        const unsigned long long span = (unsigned long long)(b + 1) << CL_BSH;
+        const uint32_t thw = (b < 0 || span >= (unsigned long long)mx) ? 1u : (uint32_t)(mx - span + 1u);
+        cs->n = 0;
+        cs->theta = thw == 1u ? 1ull : (uint64_t)thw << 32;
+        cs->valid = 1;
+      }
     }
     __syncthreads();
     mark(1);
@@ -940,7 +999,10 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
       __syncthreads();
       // the list cannot give the exact top K: a full scan this round; the list is rebuilt
       // after the publication (rebuild_after), off the path to the message
-      if (cls->need) cta_topk_scan<R, K>(trec, P.Lc, tk, wk, lane, warp, NW);
+      if (cls->need) {
+        if (prof) atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 473, 1ull);   // scans (CTA 0)
+        cta_topk_scan<R, K>(trec, P.Lc, tk, wk, lane, warp, NW);
+      }
     } else if constexpr (TOPK == 1) {
       cta_topk_scan<R, K>(trec, P.Lc, tk, wk, lane, warp, NW);
     } else {
@@ -960,7 +1022,7 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
         if (P.prof != nullptr && slot == 0 && tid == 0 && rank < 128)   // rebuilds of every CTA
           atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 320 + rank, 1ull);
         cl_rebuild<R, K>(hk, P.Lc, cls, clid, nmx, inl, lane, warp,
-                         prof ? reinterpret_cast<unsigned long long*>(P.prof) + 468 : nullptr);
+                         prof ? reinterpret_cast<unsigned long long*>(P.prof) + 468 : nullptr, !GX);
         if (prof) atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 17, (unsigned long long)(clock64() - tr0));
         if (tid == 0) {
           cls->need = 0;
