@@ -149,10 +149,13 @@ struct ClState {
   int done;                      // radix select finished
   int valid;                     // 0: the rebuild could not make an exact list (ties) -> scan
   int need;                      // 1: the list could not give the exact top K (scan), rebuild it
-  int soon;                      // 1: fewer than CL_LOW entries left -- rebuild after this publication
+  int soon;                      // 1: fewer than CL_LOW entries left -- rebuild after the publications
+  int stage;                     // staged rebuild: 0 idle, 1 node maxima taken, 2 threshold chosen
+  int pad_;
+  uint64_t pend_theta;           // staged rebuild: the chosen threshold (order key)
 };
 #ifndef MPG_CL_LOW
-#define MPG_CL_LOW 8
+#define MPG_CL_LOW 12
 #endif
 constexpr int CL_LOW = MPG_CL_LOW;   // list length below which the list is rebuilt pre-emptively
 constexpr int CL_NBK = 256;          // rebuild: buckets of node maxima below the largest
@@ -522,9 +525,15 @@ __device__ __forceinline__ uint32_t hkey(R s) {
 // overflows (one word tied more than CL_CAP times), the list is marked invalid and the
 // caller extracts by a full scan until a later rebuild succeeds.
 template <typename R, int K>
+// mode 0: the whole rebuild.  Staged over three publications (1, 2, 3), each short enough
+// to hide in the CTA's wait for its peers' messages while the old list keeps serving:
+// 1 node maxima (and their histogram), 2 the threshold for CL_TARGET into pend_theta (the
+// node maxima may be a round old: only a choice of threshold), 3 the gather of every tile
+// word >= it over ALL nodes (current words: the invariant), replacing the old list; an
+// overflow there leaves the list invalid and the next extraction falls back to mode 0.
 __device__ __noinline__ void cl_rebuild(const uint32_t* hk, long long Lc, ClState* cs, int* clid, uint32_t* nm,
                                         unsigned char* inl, int lane, int warp, unsigned long long* pf,
-                                        bool hist_first) {
+                                        bool hist_first, int mode) {
   const int tid = threadIdx.x, nthr = blockDim.x, NW = nthr >> 5;
   const int nn = (int)((Lc + 31) >> 5);
   // profile (pf != null on thread 0 of CTA 0): [0] node maxima, [1] thresholds, [2] gathers,
@@ -537,12 +546,55 @@ __device__ __noinline__ void cl_rebuild(const uint32_t* hk, long long Lc, ClStat
       tp = tn;
     }
   };
-  if (pf) atomicAdd(pf + 4, 1ull);
+  if (pf && mode <= 1) atomicAdd(pf + 4, 1ull);
   uint32_t* hist = nm + nn;   // [CL_NBK] node counts per bucket, [CL_NBK] = the largest node maximum
-  {  // the old list's membership flags (inl[l] = 1 exactly for the stored entries)
+  if (mode == 3) {            // staged gather: every current word >= the pending threshold
+    const uint64_t tpend = cs->pend_theta;
+    const uint32_t thw = tpend == 1ull ? 1u : (uint32_t)(tpend >> 32);
+    {
+      const int n0 = min(cs->n, CL_CAP);
+      for (int i = tid; i < n0; i += nthr) inl[clid[i]] = 0;
+    }
+    __syncthreads();
+    if (tid == 0) cs->n = 0;
+    __syncthreads();
+    for (int q = warp; q < nn; q += NW) {
+      const long long i = (long long)q * 32 + lane;
+      const bool in = i < Lc && hk[i] >= thw;
+      const unsigned m = __ballot_sync(0xffffffffu, in);
+      if (m == 0u) continue;   // (warp-uniform)
+      int base = 0;
+      if (lane == 0) base = atomicAdd(&cs->n, __popc(m));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      const int idx = base + __popc(m & ((1u << lane) - 1u));
+      if (in && idx < CL_CAP) {
+        clid[idx] = (int)i;
+        inl[i] = 1;
+      }
+    }
+    __syncthreads();
+    mark(2);
+    if (cs->n <= CL_CAP) {
+      if (tid == 0) {
+        cs->theta = tpend;
+        cs->valid = 1;
+      }
+      __syncthreads();
+      return;
+    }
+    // overflow (the threshold was chosen on older node maxima): unmark the stored entries
+    // and rebuild in full now
+    for (int i = tid; i < CL_CAP; i += nthr) inl[clid[i]] = 0;
+    __syncthreads();
+    if (tid == 0) cs->n = 0;
+    __syncthreads();
+    mode = 0;
+  }
+  if (mode == 0) {  // the old list's membership flags (inl[l] = 1 exactly for the stored entries)
     const int n0 = min(cs->n, CL_CAP);
     for (int i = tid; i < n0; i += nthr) inl[clid[i]] = 0;
   }
+  if (mode <= 1) {
   for (int b = tid; b <= CL_NBK; b += nthr) hist[b] = 0u;
   __syncthreads();
   {
@@ -559,23 +611,35 @@ __device__ __noinline__ void cl_rebuild(const uint32_t* hk, long long Lc, ClStat
   mark(0);
   // node maxima by bucket below the largest: (mx - m) >> CL_BSH, the last bucket holding
   // everything further down (one shared atomic per node)
-  const uint32_t mx = hist[CL_NBK];
   if (hist_first) {
+    const uint32_t mx1 = hist[CL_NBK];
     for (int q = tid; q < nn; q += nthr) {
       const uint32_t m = nm[q];
-      if (m != 0u) atomicAdd(&hist[min((mx - m) >> CL_BSH, (uint32_t)(CL_NBK - 1))], 1u);
+      if (m != 0u) atomicAdd(&hist[min((mx1 - m) >> CL_BSH, (uint32_t)(CL_NBK - 1))], 1u);
     }
     __syncthreads();
   }
-  for (int T = CL_TARGET;; T >>= 1) {
-    if (T < CL_TARGET || !hist_first) {
+  if (mode == 1) return;
+  }
+  const uint32_t mx = hist[CL_NBK];
+  // the threshold goes to the live list (mode 0) or to the pending one (mode 2, the live
+  // list keeps serving until the gather)
+  uint64_t* thp = mode == 2 ? &cs->pend_theta : &cs->theta;
+  // first target: CL_TARGET, at most half the nodes (small slices, C1: a target above the
+  // node count makes every positive word the list, which overflows) -- unless the whole
+  // slice fits the list (C0: every positive word, no rebuild again)
+  const int T0 = Lc <= CL_CAP ? CL_TARGET : min(CL_TARGET, max(1, nn >> 1));
+  for (int T = T0;; T >>= 1) {
+    if (T < T0 || !hist_first) {
       // the exact node maximum of rank T-1, by a rank count over the nodes (two threads per
       // node, ties by node index): after an overflow (crowded bucket), and for the grid
       // kernels (C4: its late rounds' crowded buckets overflow often, 5.03 -> 5.08 us/atom)
       if (tid == 0) {
-        cs->n = 0;
-        cs->theta = 1ull;   // (no node of rank T-1 with a positive maximum: every positive word)
-        cs->valid = 1;
+        if (mode != 2) {
+          cs->n = 0;
+          cs->valid = 1;
+        }
+        *thp = 1ull;   // (no node of rank T-1 with a positive maximum: every positive word)
       }
       __syncthreads();
       for (int t2 = tid; t2 < 2 * ((nn + 15) & ~15); t2 += nthr) {
@@ -598,7 +662,7 @@ __device__ __noinline__ void cl_rebuild(const uint32_t* hk, long long Lc, ClStat
         }
         int r = r0 + r1 + r2 + r3;
         r += __shfl_xor_sync(0xffffffffu, r, 1);
-        if (h == 0 && t < nn && r == T - 1 && v != 0u) cs->theta = (uint64_t)v << 32;
+        if (h == 0 && t < nn && r == T - 1 && v != 0u) *thp = (uint64_t)v << 32;
       }
     } else if (warp == 0) {
       // the first bucket (below the last) at which the node count reaches T: its lower edge
@@ -629,13 +693,16 @@ __device__ __noinline__ void cl_rebuild(const uint32_t* hk, long long Lc, ClStat
       if (lane == 0) {
         const unsigned long long span = (unsigned long long)(b + 1) << CL_BSH;
         const uint32_t thw = (b < 0 || span >= (unsigned long long)mx) ? 1u : (uint32_t)(mx - span + 1u);
-        cs->n = 0;
-        cs->theta = thw == 1u ? 1ull : (uint64_t)thw << 32;
-        cs->valid = 1;
+        if (mode != 2) {
+          cs->n = 0;
+          cs->valid = 1;
+        }
+        *thp = thw == 1u ? 1ull : (uint64_t)thw << 32;
       }
     }
     __syncthreads();
     mark(1);
+    if (mode == 2) return;   // staged: the gather follows after the next publication
     const uint64_t th = cs->theta;
     const uint32_t thw = th == 1ull ? 1u : (uint32_t)(th >> 32);
     for (int q = warp; q < nn; q += NW) {
@@ -1016,17 +1083,24 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
   // The list invariant holds across it: the next items add every rewritten tile >= theta.
   auto rebuild_after = [&]() {
     if constexpr (TOPK == 2) {
-      if (cls->need | cls->soon) {   // (uniform: both written before the top-K barrier)
+      const int stg = cls->stage;
+      if (cls->need | cls->soon | stg) {   // (uniform: written before the top-K barrier)
+        // need: the whole rebuild now; else the staged one, one stage per publication
+        const int mode = cls->need ? 0 : stg + 1;
         const long long tr0 = prof ? clock64() : 0;
-        if (prof) atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 19, 1ull);
-        if (P.prof != nullptr && slot == 0 && tid == 0 && rank < 128)   // rebuilds of every CTA
+        if (prof && mode <= 1) atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 19, 1ull);
+        if (P.prof != nullptr && slot == 0 && tid == 0 && rank < 128 && mode <= 1)   // rebuilds of every CTA
           atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 320 + rank, 1ull);
         cl_rebuild<R, K>(hk, P.Lc, cls, clid, nmx, inl, lane, warp,
-                         prof ? reinterpret_cast<unsigned long long*>(P.prof) + 468 : nullptr, !GX);
+                         prof ? reinterpret_cast<unsigned long long*>(P.prof) + 468 : nullptr, !GX, mode);
         if (prof) atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 17, (unsigned long long)(clock64() - tr0));
         if (tid == 0) {
-          cls->need = 0;
-          cls->soon = 0;
+          const bool fin = mode == 0 || mode == 3;
+          cls->stage = fin ? 0 : mode;
+          if (fin) {
+            cls->need = 0;
+            cls->soon = 0;
+          }
         }
         __syncthreads();
       }
@@ -1037,6 +1111,8 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
       cls->need = 1;
       cls->valid = 1;
       cls->n = 0;
+      cls->soon = 0;
+      cls->stage = 0;
     }
     __syncthreads();
   }
