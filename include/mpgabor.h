@@ -274,7 +274,8 @@ int mpgabor_set_profile(mpgabor* h, int32_t mode);
  * cycles): counts, [456..463] their cycle sums; [464..467] rounds by the deepest
  * CTA-list position (0..3) among the walk-window entries; [468..472] candidate-list
  * rebuilds of CTA 0: node maxima, rank counts, gathers (cycles), rank-halving retries,
- * rebuilds. */
+ * rebuilds, [473] record-scan fallbacks; [480..495] all CTAs' rounds by items (8 per
+ * bucket), [496..511] by busy cycles (4096 per bucket). */
 int mpgabor_last_profile(const mpgabor* h, int64_t* cycles);
 
 void mpgabor_destroy(mpgabor* h);

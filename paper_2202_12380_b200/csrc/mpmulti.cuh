@@ -1918,6 +1918,9 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
         atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 64 + rank, busy);
         atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 192 + rank, (unsigned long long)(hi - lo));
       }
+      // every CTA's rounds by items (8 per bucket) and by busy cycles (4096 per bucket)
+      atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 480 + min((hi - lo) >> 3, 15), 1ull);
+      atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 496 + (int)min(busy >> 12, 15ull), 1ull);
     }
     if (warp == 0) publish(par ^ 1, (unsigned long long)round + 2);
     rebuild_after();

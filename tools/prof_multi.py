@@ -59,6 +59,8 @@ for name in cfgs:
         nc = max(c[472], 1)
         print(f"   rebuild split (CTA 0, cycles per rebuild): node maxima {c[468] / nc:.0f}, rank counts {c[469] / nc:.0f}, "
               f"gathers {c[470] / nc:.0f}, retries {c[471] / nc:.2f} per rebuild; record scans (list short) {c[473]}", flush=True)
+        print("   CTA-rounds by items (buckets of 8): " + " ".join(str(c[480 + i]) for i in range(16)), flush=True)
+        print("   CTA-rounds by busy cycles (buckets of 4096): " + " ".join(str(c[496 + i]) for i in range(16)), flush=True)
         print("   deepest CTA-list position in the walk window (0..3): "
               + " ".join(str(c[464 + i]) for i in range(4)), flush=True)
         mp.set_profile(0)
