@@ -3,6 +3,8 @@
 //   N1 DGT analysis, N2 Gram cross-kernel precompute + threshold +
 //   compaction (Eqs. (14)-(17); Eq. (7)), N4 tile-max init.
 #include <algorithm>
+#include <cstdint>
+#include <cstdlib>
 #include "launch.h"
 #include "fft.cuh"
 #include "argmax.cuh"
@@ -252,6 +254,266 @@ __global__ void __launch_bounds__(512) dgt_stockham_kernel(const double* __restr
 }
 
 // ---------------------------------------------------------------------------
+// The same analysis with the frame size a compile-time constant (n = 2^LGN complex
+// points, M = 2n, LGN = 4..13) for the common window shape gl <= M, gl % 4 == 0, a even
+// (every configuration of the paper and C0-C4).  The profile of the runtime-size kernel
+// above (profiles/r02an_dgt_sass_mix.md) spent 39 % of its instructions folding the
+// frame into shared memory and 43 % on the post-processing, almost all of it integer
+// index arithmetic; here
+//  * the fold is fused into the first Stockham pass: the pass's 16 inputs per thread,
+//    z[i] = (x_w[2i], x_w[2i+1]), are read straight from the signal as 16-byte pairs
+//    (gl % 4 == 0 and a even keep each pair adjacent, aligned and inside one window
+//    period), multiplied by the window pair and transformed in registers -- no
+//    shared-memory round trip and no barrier;
+//  * every index of the passes is a compile-time offset from one per-thread base;
+//  * the post-processing produces X[m] and X[n-m] from one pair of shared loads:
+//    with T = W^m O[m], X[m] = E[m] + T and X[n-m] = conj(E[m] - T)
+//    (E[n-m] = conj E[m], O[n-m] = conj O[m], W^{n-m} = -conj W^m).
+// ---------------------------------------------------------------------------
+template <int LGN>
+struct DgtC {
+  static constexpr int n = 1 << LGN, M = 2 * n;
+  static constexpr int LGTPF = LGN - 4, TPF = 1 << LGTPF;   // threads per frame (16 values each)
+  static constexpr int Q = LGN & 3;                         // first pass radix 2^Q (16 if Q == 0)
+  static constexpr int LGR0 = Q ? Q : 4;
+};
+
+// one compile-time Stockham pass (LGNS > 0: after the first), radix 2^LGR, as stockham_pass
+template <int LGN, int LGR, int LGNS, int SIGN>
+__device__ __forceinline__ void spass_ct(double2* z, int fb, int t, const double2* __restrict__ tw, int twres) {
+  constexpr int R = 1 << LGR, B = 16 >> LGR, TPF = DgtC<LGN>::TPF;
+  constexpr int QS = 1 << (LGN - LGR), NS = 1 << LGNS;
+  double2 v[B][R];
+#pragma unroll
+  for (int b = 0; b < B; ++b) {
+    const int j = t + b * TPF;
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[b][r] = z[pz(fb + j + r * QS)];
+  }
+  __syncthreads();
+  const int tws = twres >> (LGNS + LGR);
+#pragma unroll
+  for (int b = 0; b < B; ++b) {
+    const int j = t + b * TPF;
+    const int k = j & (NS - 1);
+    double2 w1 = tw_full(tw, k * tws, twres);
+    if (SIGN > 0) w1.y = -w1.y;
+    double2 wp[R];
+    wp[1] = w1;
+#pragma unroll
+    for (int r = 2; r < R; ++r) {
+      const int hb = 1 << (31 - __clz(r));
+      wp[r] = r == hb ? cmul(wp[r >> 1], wp[r >> 1]) : cmul(wp[hb], wp[r - hb]);
+    }
+#pragma unroll
+    for (int r = 1; r < R; ++r) v[b][r] = cmul(v[b][r], wp[r]);
+    reg_dft<LGR, SIGN>(v[b]);
+    const int base = ((j - k) << LGR) + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) z[pz(fb + base + r * NS)] = v[b][r];
+  }
+  __syncthreads();
+}
+
+template <int LGN, int LGNS>
+__device__ __forceinline__ void spass_rest(double2* z, int fb, int t, const double2* __restrict__ tw, int twres) {
+  if constexpr (LGNS < LGN) {
+    spass_ct<LGN, 4, LGNS, -1>(z, fb, t, tw, twres);
+    spass_rest<LGN, LGNS + 4>(z, fb, t, tw, twres);
+  }
+}
+
+#ifndef MPG_DGT_STAGE
+#define MPG_DGT_STAGE 0   // 1: the CTA's signal range staged by a TMA bulk copy (measured slower)
+#endif
+#ifndef MPG_DGT_THREADS
+#define MPG_DGT_THREADS 128   // threads per CTA (at least one frame: n/16 threads)
+#endif
+#ifndef MPG_DGT_MINB
+#define MPG_DGT_MINB 5   // resident CTAs per SM the register allocation targets (<= 102 registers)
+#endif
+template <int LGN>
+constexpr int dgt_ct_threads() { return DgtC<LGN>::TPF > MPG_DGT_THREADS ? DgtC<LGN>::TPF : MPG_DGT_THREADS; }
+template <int LGN>
+constexpr int dgt_ct_minb() { return dgt_ct_threads<LGN>() > MPG_DGT_THREADS ? 1 : MPG_DGT_MINB; }
+template <typename R, int LGN>
+__global__ void __launch_bounds__(dgt_ct_threads<LGN>(), dgt_ct_minb<LGN>()) dgt_ct_kernel(
+    const double* __restrict__ x, int64_t L, int a, int gl, int N, const double* __restrict__ g,
+    const double2* __restrict__ tw, int twres, typename cplx<R>::t* __restrict__ out, int stride, int write_pad) {
+  using C2 = typename cplx<R>::t;
+  using S = DgtC<LGN>;
+  constexpr int n = S::n, M = S::M, TPF = S::TPF, LGR0 = S::LGR0;
+  constexpr int R0 = 1 << LGR0, B0 = 16 >> LGR0, QS0 = n >> LGR0;
+  extern __shared__ double2 z[];
+  const int F = blockDim.x >> S::LGTPF;
+  const int f = threadIdx.x >> S::LGTPF, t = threadIdx.x & (TPF - 1);
+  const int frame = blockIdx.x * F + f;
+  const int fb = f << LGN;
+  // post-processing twiddles W^m, m < n/2 + 1, staged in shared memory when the table
+  // entries are scattered (twstep >= 4)
+  const int twstep = twres / M;
+  double2* wt = z + (F * n + ((F * n) >> 4));
+  const bool use_wt = twstep >= 4;
+  if (use_wt)
+    for (int m = threadIdx.x; m <= n / 2; m += blockDim.x) wt[m] = __ldg(&tw[(int64_t)m * twstep]);
+  // ---- first pass (Ns = 1, no twiddles), inputs from the signal ----
+  // The CTA's signal range [frame0 a + j0, (frame0 + F - 1) a + j0 + M) (its frames
+  // overlap M/a-fold) is staged into the frame buffer by one TMA bulk copy
+  // (cp.async.bulk, completion on an mbarrier) when it does not wrap around the signal
+  // ends; each sample then leaves HBM/L2 once per CTA instead of M/a times through L1.
+  // The pass's inputs are taken into registers before the barrier after which its
+  // outputs overwrite the staged signal.  Wrapping CTAs (the first and the last) load
+  // from global memory with the circular index.
+  {
+    const int j0 = -(gl >> 1);
+    const int frame0 = blockIdx.x * F;
+    const int nfr = min(F, N - frame0);
+    const int64_t lo = (int64_t)frame0 * a + j0;
+    const int64_t cnt = (int64_t)(nfr - 1) * a + M;   // doubles (even: 16-byte multiple)
+    const bool staged = MPG_DGT_STAGE && lo >= 0 && lo + cnt <= L;    // (uniform over the CTA)
+    __shared__ alignas(8) unsigned long long xbar;
+    if (staged) {
+      if (threadIdx.x == 0) {
+        mpcore::mbar_init(mpcore::smem_addr(&xbar), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        mpcore::mbar_arm(mpcore::smem_addr(&xbar), (uint32_t)(cnt * 8));
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         mpcore::smem_addr(z)),
+                     "l"(x + lo), "r"((uint32_t)(cnt * 8)), "r"(mpcore::smem_addr(&xbar))
+                     : "memory");
+      }
+      __syncthreads();
+      mpcore::mbar_wait(mpcore::smem_addr(&xbar), 0);
+    }
+    const int64_t base = (int64_t)min(frame, N - 1) * a;
+    const bool fok = frame < N;
+    const double2* x2 = reinterpret_cast<const double2*>(x);
+    const double2* xs = reinterpret_cast<const double2*>(z) + ((f * a) >> 1);   // staged frame f
+    const double2* g2 = reinterpret_cast<const double2*>(g);
+    double2 v[B0][R0];
+#pragma unroll
+    for (int b = 0; b < B0; ++b) {
+      const int j = t + b * TPF;
+#pragma unroll
+      for (int r = 0; r < R0; ++r) {
+        const int i = j + r * QS0;
+        const int jw = (2 * i - j0) & (M - 1);     // window index of sample 2i (even)
+        const bool ok = fok && jw < gl;
+        double2 xv;
+        if (staged) {
+          xv = ok ? xs[jw >> 1] : make_double2(0.0, 0.0);
+        } else {
+          int64_t pos = base + j0 + jw;
+          pos += pos < 0 ? L : 0;
+          pos -= pos >= L ? L : 0;
+          xv = ok ? __ldg(&x2[pos >> 1]) : make_double2(0.0, 0.0);
+        }
+        const double2 gv = ok ? __ldg(&g2[jw >> 1]) : make_double2(0.0, 0.0);
+        v[b][r] = make_double2(xv.x * gv.x, xv.y * gv.y);
+      }
+    }
+    __syncthreads();   // every input is in registers: the staged signal may be overwritten
+#pragma unroll
+    for (int b = 0; b < B0; ++b) {
+      const int j = t + b * TPF;
+      reg_dft<LGR0, -1>(v[b]);
+#pragma unroll
+      for (int r = 0; r < R0; ++r) z[pz(fb + (j << LGR0) + r)] = v[b][r];
+    }
+    __syncthreads();
+  }
+  spass_rest<LGN, LGR0>(z, fb, t, tw, twres);
+  // ---- X[m], X[n-m] for m = t + k TPF < n/2; X[n/2] by thread 0; zero padding ----
+  if (frame >= N) return;
+  C2* orow = out + (int64_t)frame * stride;
+  const double2* zf = z + pz(fb);   // (fb is a multiple of 16: pz(fb + i) = pz(fb) + pz(i))
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int m = t + k * TPF;
+    const double2 Zm = zf[pz(m)];
+    const double2 Zc = cconj(zf[pz((n - m) & (n - 1))]);
+    const double2 E = make_double2(0.5 * (Zm.x + Zc.x), 0.5 * (Zm.y + Zc.y));
+    const double2 D = csub(Zm, Zc);
+    const double2 O = make_double2(0.5 * D.y, -0.5 * D.x);
+    const double2 W = use_wt ? wt[m] : __ldg(&tw[(int64_t)m * twstep]);
+    const double2 T = cmul(W, O);
+    C2 o1, o2;
+    o1.x = (R)(E.x + T.x);
+    o1.y = (R)(E.y + T.y);
+    o2.x = (R)(E.x - T.x);
+    o2.y = (R)(T.y - E.y);
+    orow[m] = o1;
+    orow[n - m] = o2;
+  }
+  if (t == 0) {
+    const int m = n / 2;
+    const double2 Zm = zf[pz(m)];
+    const double2 Zc = cconj(Zm);
+    const double2 E = make_double2(0.5 * (Zm.x + Zc.x), 0.5 * (Zm.y + Zc.y));
+    const double2 D = csub(Zm, Zc);
+    const double2 O = make_double2(0.5 * D.y, -0.5 * D.x);
+    const double2 W = use_wt ? wt[m] : __ldg(&tw[(int64_t)m * twstep]);
+    const double2 X = cadd(E, cmul(W, O));
+    C2 o;
+    o.x = (R)X.x;
+    o.y = (R)X.y;
+    orow[m] = o;
+  }
+  if (write_pad)
+    for (int m = n + 1 + t; m < stride; m += TPF) {
+      C2 o;
+      o.x = 0;
+      o.y = 0;
+      orow[m] = o;
+    }
+}
+
+template <typename R, int LGN>
+static cudaError_t launch_dgt_ct(const double* xp, int64_t L, const DictGeo& d, const double* g, const double2* tw,
+                                 int twres, typename cplx<R>::t* out, cudaStream_t st, int write_pad) {
+  using S = DgtC<LGN>;
+  const int threads = dgt_ct_threads<LGN>();
+  const int F = threads / S::TPF;
+  const int n = S::n;
+  const bool use_wt = twres / S::M >= 4;
+  const size_t smem = (size_t)(F * n + (F * n) / 16 + (use_wt ? n / 2 + 1 : 0)) * sizeof(double2);
+  static bool attr = false;
+  if (!attr) {
+    // (<= 140 KB for every LGN; the kernel has 16 bytes of static shared memory besides)
+    CUDA_OK(cudaFuncSetAttribute(dgt_ct_kernel<R, LGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+    attr = true;
+  }
+  dgt_ct_kernel<R, LGN><<<(d.N + F - 1) / F, threads, smem, st>>>(xp, L, d.a, d.gl, d.N, g, tw, twres, out, d.stride,
+                                                                  write_pad);
+  return cudaGetLastError();
+}
+
+// the compile-time kernel applies: gl <= M, gl % 4 == 0, a even, 16-byte aligned x and g
+static bool dgt_ct_applies(const double* xp, const DictGeo& d, const double* g) {
+  return d.M >= 32 && d.M <= 16384 && d.gl <= d.M && d.gl % 4 == 0 && d.a % 2 == 0 &&
+         ((uintptr_t)xp & 15) == 0 && ((uintptr_t)g & 15) == 0;
+}
+
+template <typename R>
+static cudaError_t launch_dgt_ct_any(const double* xp, int64_t L, const DictGeo& d, const double* g,
+                                     const double2* tw, int twres, typename cplx<R>::t* out, cudaStream_t st,
+                                     int write_pad) {
+  switch (31 - __builtin_clz((unsigned)d.M / 2)) {
+    case 4: return launch_dgt_ct<R, 4>(xp, L, d, g, tw, twres, out, st, write_pad);
+    case 5: return launch_dgt_ct<R, 5>(xp, L, d, g, tw, twres, out, st, write_pad);
+    case 6: return launch_dgt_ct<R, 6>(xp, L, d, g, tw, twres, out, st, write_pad);
+    case 7: return launch_dgt_ct<R, 7>(xp, L, d, g, tw, twres, out, st, write_pad);
+    case 8: return launch_dgt_ct<R, 8>(xp, L, d, g, tw, twres, out, st, write_pad);
+    case 9: return launch_dgt_ct<R, 9>(xp, L, d, g, tw, twres, out, st, write_pad);
+    case 10: return launch_dgt_ct<R, 10>(xp, L, d, g, tw, twres, out, st, write_pad);
+    case 11: return launch_dgt_ct<R, 11>(xp, L, d, g, tw, twres, out, st, write_pad);
+    case 12: return launch_dgt_ct<R, 12>(xp, L, d, g, tw, twres, out, st, write_pad);
+    case 13: return launch_dgt_ct<R, 13>(xp, L, d, g, tw, twres, out, st, write_pad);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // N2 kernel rows: for lag nu = nu_first + blockIdx.x
 //   b[s mod M_c] += g_u(s + nu a_c) g_v(s),  H[i][m] = sum_s b e^{-2 pi i m s/M_c}, m = 0..M_c/2
 // i.e. h_{u,v}(m, nu) for m >= 0 (h(-m,nu) = conj h(m,nu), real windows).
@@ -470,6 +732,11 @@ static int dgt_frames_per_cta(int M) { return max(1, 4096 / (M / 2)); }
 template <typename R>
 cudaError_t launch_dgt(const double* xp, int64_t L, const DictGeo& d, const double* g, const double2* tw,
                        int twres, typename cplx<R>::t* out, cudaStream_t st, int write_pad) {
+  // the compile-time-size kernel where it applies (MPGABOR_DGT_RT=1: the runtime-size
+  // kernels below, kept for every other window shape and as the tests' second path)
+  const char* rt = std::getenv("MPGABOR_DGT_RT");
+  if (!(rt != nullptr && rt[0] == '1') && dgt_ct_applies(xp, d, g))
+    return launch_dgt_ct_any<R>(xp, L, d, g, tw, twres, out, st, write_pad);
   if (d.M >= 32) {  // Stockham: n/16 threads per frame, >= 256 threads per CTA
     const int tpf = d.M / 32;
     int F = std::max(1, 256 / tpf);

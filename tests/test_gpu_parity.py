@@ -134,9 +134,10 @@ def test_dgt_matches_oracle(mpg, name, prec):
     mp.close()
 
 
-# every channel count M the library takes (Z25) through both DGT kernels: the radix-2
+# every channel count M the library takes (Z25) through every DGT kernel: the radix-2
 # kernel (M < 32) and the register-blocked Stockham FFT (M >= 32: radix-2/4/8 first pass,
-# then radix-16 passes), redundancies 4 and 8, a window shorter than M and one longer
+# then radix-16 passes) in its runtime-size and compile-time-size forms, redundancies 4
+# and 8, a window shorter than M and one longer
 DGT_DICTS = ([Dict(BLACKMAN, M, max(1, M // 4), M) for M in (2, 4, 8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096,
                                                               8192, 16384)]
              + [Dict(BLACKMAN, M, M // 8, M) for M in (32, 256, 2048, 16384)]
@@ -144,9 +145,13 @@ DGT_DICTS = ([Dict(BLACKMAN, M, max(1, M // 4), M) for M in (2, 4, 8, 16, 32, 64
              + [Dict(GAUSS, 97, 16, 64)])
 
 
+# kernel "ct": the compile-time-size kernel (gl <= M, gl % 4 == 0, a even; the others fall
+# back to the runtime-size kernels); "rt": MPGABOR_DGT_RT=1 forces the runtime-size kernels
+@pytest.mark.parametrize("kernel", ["ct", "rt"])
 @pytest.mark.parametrize("prec", ["f64", "f32"])
 @pytest.mark.parametrize("d", DGT_DICTS, ids=lambda d: f"w{d.win}gl{d.gl}a{d.a}M{d.M}")
-def test_dgt_every_channel_count(mpg, d, prec):
+def test_dgt_every_channel_count(mpg, d, prec, kernel, monkeypatch):
+    monkeypatch.setenv("MPGABOR_DGT_RT", "1" if kernel == "rt" else "0")
     x = random_signal(65536 - 77, 5)      # ragged: zero-padded to a multiple of lcm(a, M)
     S = oracle.Setup.build(x, (d,), 1e-4)
     mp, out, _ = gpu_run(mpg, (d,), 1e-4, x, 0, -math.inf, prec)
