@@ -244,7 +244,10 @@ def run_reference(args, cfg, rank, world):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": workload_desc(cfg, "f64"), "parallelism": "cpu-1thread"},
+            "data": "synthetic",
+            "config": {"workload": workload_desc(cfg, "f64"),
+                       "step": "DGT + MP loop to the stop rule + synthesis (dgtrealmp_execute); kernels per handle",
+                       "iterations_per_step": iters // max(args.steps, 1), "parallelism": "cpu-1thread"},
             "cpu_baseline": baseline_record(value, sum(p["loop_s"] for p in parts), iters, sample),
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "phases_s": {k: float(np.mean([p[k] for p in parts])) for k in parts[0]}}

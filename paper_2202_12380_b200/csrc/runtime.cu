@@ -108,6 +108,11 @@ struct mpgabor {
   long long prof_host[MPG_PROF_SLOTS] = {};
   DevBuf prof;
   cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  // DGT fork/join: the W dictionaries' analysis kernels run on side streams so that one
+  // kernel's tail waves overlap the next kernel's first (MPGABOR_DGT_STREAMS=0: in line)
+  cudaStream_t dgt_st[MPG_MAX_DICTS] = {};
+  cudaEvent_t dgt_fork = nullptr, dgt_join[MPG_MAX_DICTS] = {};
+  int dgt_streams = -1;   // -1 not decided, 0 off, 1 on
   float t_dgt = 0, t_init = 0, t_loop = 0;
   int64_t launches = 0;  // kernels of this library enqueued through this handle
 
@@ -136,6 +141,25 @@ struct mpgabor {
     TRY_CUDA(h, expr);         \
     (h)->launches += (n);      \
   } while (0)
+
+// side streams for the DGT fork/join, created on first use (after enter_device)
+static bool dgt_side_streams(mpgabor* h) {
+  if (h->dgt_streams < 0) {
+    const char* e = getenv("MPGABOR_DGT_STREAMS");
+    h->dgt_streams = (e && e[0] == '0') ? 0 : 1;
+    if (h->dgt_streams) {
+      bool ok = cudaEventCreateWithFlags(&h->dgt_fork, cudaEventDisableTiming) == cudaSuccess;
+      for (int w = 1; ok && w < h->W; ++w)
+        ok = cudaStreamCreateWithFlags(&h->dgt_st[w], cudaStreamNonBlocking) == cudaSuccess &&
+             cudaEventCreateWithFlags(&h->dgt_join[w], cudaEventDisableTiming) == cudaSuccess;
+      if (!ok) {
+        (void)cudaGetLastError();
+        h->dgt_streams = 0;
+      }
+    }
+  }
+  return h->dgt_streams == 1;
+}
 
 static int enter_device(mpgabor* h) {
   if (h->device < 0) {
@@ -213,6 +237,11 @@ extern "C" void mpgabor_destroy(mpgabor* h) {
       b->release();
     for (auto e : h->ev)
       if (e) cudaEventDestroy(e);
+    for (auto e : h->dgt_join)
+      if (e) cudaEventDestroy(e);
+    if (h->dgt_fork) cudaEventDestroy(h->dgt_fork);
+    for (auto s2 : h->dgt_st)
+      if (s2) cudaStreamDestroy(s2);
   }
   delete h;
 }
@@ -813,17 +842,26 @@ static int run_impl(mpgabor* h, const double* x_dev, int64_t Ls, int64_t maxit, 
     const int write_pad = b >= h->pad_clean ? 1 : 0;
     TRY_LAUNCH(h, 2, launch_pad_energy(x_dev + (int64_t)b * Ls, Ls, h->xp.as<double>(), h->L, h->partial.as<double>(),
                                        h->flag.as<int>(), h->E0.as<double>() + b, st));
+    const bool fork = dgt_side_streams(h) && W > 1;
+    if (fork) TRY_CUDA(h, cudaEventRecord(h->dgt_fork, st));
     for (int w = 0; w < W; ++w) {
       const DictGeo& d = h->geo[w];
       const double* g = h->win.as<double>() + h->win_off[w];
       const int64_t goff = d.grid_off + (int64_t)b * h->grid_elems;
+      // dictionary 0 stays on the caller's stream; the others fork off it and join back
+      // (the next signal's padding rewrites xp, the tile init reads every grid)
+      cudaStream_t sw = fork && w > 0 ? h->dgt_st[w] : st;
+      if (sw != st) TRY_CUDA(h, cudaStreamWaitEvent(sw, h->dgt_fork, 0));
       if (h->f64())
         TRY_LAUNCH(h, 1, launch_dgt<double>(h->xp.as<double>(), h->L, d, g, h->tw.as<double2>(), h->twres,
-                                            h->grid.as<double2>() + goff, st, write_pad));
+                                            h->grid.as<double2>() + goff, sw, write_pad));
       else
         TRY_LAUNCH(h, 1, launch_dgt<float>(h->xp.as<double>(), h->L, d, g, h->tw.as<double2>(), h->twres,
-                                           h->grid.as<float2>() + goff, st, write_pad));
+                                           h->grid.as<float2>() + goff, sw, write_pad));
+      if (sw != st) TRY_CUDA(h, cudaEventRecord(h->dgt_join[w], sw));
     }
+    if (fork)
+      for (int w = 1; w < W; ++w) TRY_CUDA(h, cudaStreamWaitEvent(st, h->dgt_join[w], 0));
   }
   h->pad_clean = std::max(h->pad_clean, B);
   TRY_CUDA(h, cudaEventRecord(h->ev[1], st));

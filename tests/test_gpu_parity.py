@@ -489,6 +489,22 @@ def test_tiny_dictionaries(mpg, dicts, Ls, thr, batch):
     mp.close()
 
 
+@pytest.mark.parametrize("batch", [1, 8])
+@pytest.mark.parametrize("C", [32, 64, 128])
+@pytest.mark.parametrize("dicts,Ls", TINY[:2])
+def test_tiny_dictionaries_grid_mode(mpg, dicts, Ls, C, batch):
+    # grid mode with fewer frames than CTAs (TINY[0]: 72 frames, TINY[1]: 150 over 3
+    # dictionaries): some CTAs own no frame, their published lists are empty, and the
+    # two-stage window ranking must still fill every window slot with a valid entry
+    x = random_signal(Ls, 11)
+    S = oracle.Setup.build(x, dicts, 1e-4)
+    ref = oloop.mp_run(S, 150, -60.0)
+    mp, out, idx = gpu_run(mpg, dicts, 1e-4, x, 150, -60.0, "f64", launch=(C, 0, 0, 0), batch=batch)
+    assert mp.launch_info()["cluster"] == C
+    assert_fp64_parity(out, idx, ref)
+    mp.close()
+
+
 def test_planted_atoms_recovered_c0(mpg):
     # C0: the 20 planted unit atoms dominate; the first selections find planted (m, n)
     cfg = CONFIGS["C0"]
