@@ -410,6 +410,37 @@ def test_deterministic(mpg):
     mp.close()
 
 
+@pytest.mark.parametrize("fork", ["1", "0"])
+def test_user_stream_and_dgt_side_streams(mpg, fork, monkeypatch):
+    # the DGT of the W dictionaries forks over side streams and joins the caller's stream
+    # (runtime.cu dgt_side_streams; MPGABOR_DGT_STREAMS=0: launched in line): the run on a
+    # user stream that is busy when the call is made equals the default-stream run bit for
+    # bit, in both modes, and repeated runs reuse the side streams
+    monkeypatch.setenv("MPGABOR_DGT_STREAMS", fork)
+    cfg = CONFIGS["C2"]
+    x, S = setup_of("C2")
+    xd = torch.from_numpy(x).cuda()
+    mp = mpg.MPGabor(cfg.dicts, cfg.thr, "f64")
+    ref = mp.run(xd, 2000, cfg.errdb)
+    res_ref = mp.residual(cfg.Ls).cpu().numpy()
+    st = torch.cuda.Stream()
+    st.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(st):
+        for _ in range(3):
+            junk = torch.empty(64 << 20, dtype=torch.uint8, device="cuda").fill_(1)   # keeps the stream busy
+            xs = xd.clone()            # produced on the user stream right before the call
+            out = mp.run(xs, 2000, cfg.errdb)
+            res = mp.residual(cfg.Ls)
+            st.synchronize()
+            assert out.atoms.tobytes() == ref.atoms.tobytes() and out.energy.tobytes() == ref.energy.tobytes()
+            assert np.array_equal(res.cpu().numpy(), res_ref)
+            del junk
+    torch.cuda.current_stream().wait_stream(st)
+    ro = ref_of("C2", 2000)
+    assert_fp64_parity(ref, ref.index(S.lay.off, S.lay.MR), ro)
+    mp.close()
+
+
 def test_decompose_host_matches_device(mpg):
     cfg = CONFIGS["C1"]
     x, S = setup_of("C1")
