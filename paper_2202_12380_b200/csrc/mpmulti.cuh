@@ -66,6 +66,9 @@ using namespace mpcore;
 #ifndef MPG_LB_THREADS
 #define MPG_LB_THREADS 512  // launch bound (max threads per CTA; 256 leaves 255 registers per thread)
 #endif
+#ifndef MPG_SCAN_W1
+#define MPG_SCAN_W1 1     // the round's item bases by warp 1 while warp 0 runs the energy chain
+#endif
 #ifndef MPG_ECHAIN_BF
 #define MPG_ECHAIN_BF 1   // the round's energy chain without branches (0: the branching form)
 #endif
@@ -109,6 +112,7 @@ struct St {               // round state (shared memory)
   long long it;           // accepted atoms
   double Enext[BMAX];     // E after candidate g
   int G;                  // candidates of the round just run (verified by the next round)
+  int Gw;                 // picks of the walk before the energy stop rules (>= G; warp 1's item bases)
   int mode;               // 0 select, 1 roll back candidates rb_from..G-1
   int rb_from;
   int stop;
@@ -1467,6 +1471,57 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
           }
         }
       }
+      auto item_scan = [&](int Gsc) {
+          // this CTA's items (tile pairs of its rows) and tiles of (g, v), at index
+          // t = g * 16 + v (g-major; v >= W contribute nothing): lane handles IPL pairs
+          const int GW = Gsc * 16;
+          int r4[IPL], t4[IPL], rs = 0, ts = 0;
+          // a lane's IPL entries share one candidate g (16 % IPL == 0): its window position
+          const int pq = st->pick[((lane * IPL) >> 4) & (BMAX - 1)];
+#pragma unroll
+          for (int q = 0; q < IPL; ++q) {
+            const int t = lane * IPL + q;
+            int nrw = 0, ntl = 0;
+            const int v = t & 15;
+            if (t < GW && v < W && !floorm) {
+              const int2 cn2 = ecnt[pq * 16 + v];
+              nrw = cn2.x;
+              ntl = cn2.y;
+            }
+            r4[q] = nrw;
+            t4[q] = ntl;
+            rs += nrw;
+            ts += ntl;
+          }
+          int ri = rs, ti = ts;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y1 = __shfl_up_sync(0xffffffffu, ri, o), y2 = __shfl_up_sync(0xffffffffu, ti, o);
+            if (lane >= o) {
+              ri += y1;
+              ti += y2;
+            }
+          }
+          int rr = ri - rs, tt = ti - ts;
+#pragma unroll
+          for (int q = 0; q < IPL; ++q) {
+            const int t = lane * IPL + q;
+            if (t <= GW) {
+              st->ibase[t] = rr;
+              st->tbase[t] = tt;
+            }
+            rr += r4[q];
+            tt += t4[q];
+          }
+          if (lane == 31 && GW == BMAX * 16) {
+            st->ibase[GW] = ri;
+            st->tbase[GW] = ti;
+          }
+      };
+      if (MPG_SCAN_W1 && warp == 1) {   // (NW >= 2) waits for the walk's picks, then the item bases
+        bar_sync(1, 64);
+        item_scan(st->Gw);
+      }
       if (warp == 0) {
         const bool have = lane < NEc;
         const Ent& el = ent[have ? lane : 0];   // decoded in the geometry phase
@@ -1536,6 +1591,15 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
         // E recurrence and the energy stop rules (Z15) in selection order, every lane
         // redundantly on the shuffled E~ of the picks
         if (lane < G) st->pick[lane] = pl;
+        // the item bases depend on the picks only: warp 1 computes them (for the walk's G; a
+        // stop rule can only shorten the round, and the bases of a prefix are a prefix)
+        // while this warp runs the energy chain
+        // (every launch has at least 4 warps: runtime.cu set_launch)
+#if MPG_SCAN_W1
+        if (lane == 0) st->Gw = G;
+        __syncwarp();
+        bar_sync(1, 64);
+#endif
         // (latency-floor mode: no update, so no energy change either -- E~ taken as 0)
         const double Etg = floorm ? 0.0 : __shfl_sync(0xffffffffu, Etl, pl);
         const uint32_t kmine = __shfl_sync(0xffffffffu, keyl, pl);
@@ -1604,51 +1668,9 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
           energy_out[it0 + lane + 1] = Emine;
         }
         PROF_MARK(28);
-        // this CTA's items (tile pairs of its rows) and tiles of (g, v), at index
-        // t = g * 16 + v (g-major; v >= W contribute nothing): lane handles IPL pairs
-        const int GW = G * 16;
-        int r4[IPL], t4[IPL], rs = 0, ts = 0;
-        // a lane's IPL entries share one candidate g (16 % IPL == 0): its window position
-        const int pq = __shfl_sync(0xffffffffu, pl, ((lane * IPL) >> 4) & 31);
-#pragma unroll
-        for (int q = 0; q < IPL; ++q) {
-          const int t = lane * IPL + q;
-          int nrw = 0, ntl = 0;
-          const int v = t & 15;
-          if (t < GW && v < W && !floorm) {
-            const int2 cn2 = ecnt[pq * 16 + v];
-            nrw = cn2.x;
-            ntl = cn2.y;
-          }
-          r4[q] = nrw;
-          t4[q] = ntl;
-          rs += nrw;
-          ts += ntl;
-        }
-        int ri = rs, ti = ts;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y1 = __shfl_up_sync(0xffffffffu, ri, o), y2 = __shfl_up_sync(0xffffffffu, ti, o);
-          if (lane >= o) {
-            ri += y1;
-            ti += y2;
-          }
-        }
-        int rr = ri - rs, tt = ti - ts;
-#pragma unroll
-        for (int q = 0; q < IPL; ++q) {
-          const int t = lane * IPL + q;
-          if (t <= GW) {
-            st->ibase[t] = rr;
-            st->tbase[t] = tt;
-          }
-          rr += r4[q];
-          tt += t4[q];
-        }
-        if (lane == 31 && GW == BMAX * 16) {
-          st->ibase[GW] = ri;
-          st->tbase[GW] = ti;
-        }
+#if !MPG_SCAN_W1
+        item_scan(G);
+#endif
       }
       PROF_MARK(9);
       __syncthreads();
