@@ -66,6 +66,9 @@ using namespace mpcore;
 #ifndef MPG_LB_THREADS
 #define MPG_LB_THREADS 512  // launch bound (max threads per CTA; 256 leaves 255 registers per thread)
 #endif
+#ifndef MPG_PUSH_WARPS
+#define MPG_PUSH_WARPS 1  // publication: one 16-byte chunk per thread over the first warps (0: warp 0 alone)
+#endif
 #ifndef MPG_SCAN_W1
 #define MPG_SCAN_W1 1     // the round's item bases by warp 1 while warp 0 runs the energy chain
 #endif
@@ -1017,23 +1020,29 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
     tprev = tn;                                                                                           \
   }
 
-  // warp 0: push the message (top-K records + per-candidate maxima) into slot
-  // `slot` of every CTA
-  auto publish = [&](int ps, unsigned long long stamp) {
+  // The message (top-K records + per-candidate maxima): warp 0 forms it in shared memory
+  // (form_msg, before the top-K's closing barrier), then the first warps push it into slot
+  // `ps` of every CTA, one 16-byte chunk per thread (push_msg; MPG_PUSH_WARPS = 0: warp 0
+  // alone, 5 stores per lane -- 578 cycles of every round)
+  auto form_msg = [&](unsigned long long stamp) {
     if (lane < K) mymsg->list[lane] = tk[lane] >= 0 ? trec[tk[lane]] : empty_rec(R(0));
 #ifdef MPG_CHECKS
     if (lane == 0) mymsg->tag = (uint32_t)stamp;
+#else
+    (void)stamp;
 #endif
     if (lane < BMAX) {
       mymsg->vkey[lane] = vkey[lane];
       vkey[lane] = 0;
     }
     __syncwarp();
+  };
+  auto push_msg = [&](int ps, unsigned long long stamp) {
     PROF_MARK(13);
     const int NCHUNK = (int)(msgbytes / 16);
     const uint4* src = reinterpret_cast<const uint4*>(mymsg);
     if constexpr (GX) {  // message, then its stamp (release, same thread): round `stamp - 1` may read it
-      if (lane == 0) {
+      if (tid == 0) {
         uint4* dstg = reinterpret_cast<uint4*>(reinterpret_cast<MsgT*>(P.gx_rec) + (long long)ps * C + rank);
 #pragma unroll
         for (int ch = 0; ch < (int)(sizeof(MsgT) / 16); ++ch) dstg[ch] = src[ch];
@@ -1051,7 +1060,11 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
       (void)stamp;
       const uint32_t dst = smem_addr(&mail[ps * MAX_CLUSTER + rank]);
       const uint32_t bar = smem_addr(&mbar[ps]);
-      for (int t = lane; t < C * NCHUNK; t += 32) {
+#if MPG_PUSH_WARPS
+      for (int t = tid; t < C * NCHUNK; t += blockDim.x) {
+#else
+      for (int t = warp == 0 ? lane : C * NCHUNK; t < C * NCHUNK; t += 32) {
+#endif
         const int d = t / NCHUNK, ch = t - d * NCHUNK;
         st_async16(mapa(dst + 16 * ch, d), mapa(bar, d), src[ch]);
       }
@@ -1059,12 +1072,13 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
     PROF_MARK(14);
   };
   // this CTA's K best tiles into tk[0..K-1] (all threads; a barrier before, ends with one)
-  auto topk = [&]() {
+  auto topk = [&](unsigned long long stamp) {
     if constexpr (TOPK == 2) {
       const long long tx0 = prof ? clock64() : 0;
       if (warp == 0) {
         const bool ok = cls->valid && !cls->need && cl_extract<R, K>(trec, cls, clid, inl, tk, lane);
         if (lane == 0) cls->need = ok ? 0 : 1;
+        if (ok) form_msg(stamp);
       }
       if (prof) atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 16, (unsigned long long)(clock64() - tx0));
       __syncthreads();
@@ -1073,11 +1087,14 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
       if (cls->need) {
         if (prof) atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 473, 1ull);   // scans (CTA 0)
         cta_topk_scan<R, K>(trec, P.Lc, tk, wk, lane, warp, NW);
+        if (warp == 0) form_msg(stamp);
+        __syncthreads();
       }
-    } else if constexpr (TOPK == 1) {
-      cta_topk_scan<R, K>(trec, P.Lc, tk, wk, lane, warp, NW);
     } else {
-      cta_topk<R, K>(P, lev, trec, tk, lane, warp, NW);
+      if constexpr (TOPK == 1) cta_topk_scan<R, K>(trec, P.Lc, tk, wk, lane, warp, NW);
+      else cta_topk<R, K>(P, lev, trec, tk, lane, warp, NW);
+      if (warp == 0) form_msg(stamp);
+      __syncthreads();
     }
   };
   // candidate lists: rebuild after the message is out (all threads) when the extraction ran
@@ -1120,8 +1137,8 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
     }
     __syncthreads();
   }
-  topk();
-  if (warp == 0) publish(0, 1ull);
+  topk(1ull);
+  push_msg(0, 1ull);
   rebuild_after();
 
   long long rounds = 0;
@@ -1932,7 +1949,7 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
       for (int l = 0; l < P.nlev; ++l) cnt[l] = 0;
       if (mode == 1) st->G = 0;  // nothing to verify after a roll-back
     }
-    topk();
+    topk((unsigned long long)round + 2);
     if (P.prof != nullptr && slot == 0 && tid == 0) {  // per-CTA busy time (receive -> publish) and items
       const unsigned long long busy = (unsigned long long)(clock64() - tbusy0);
       if (rank < 16) atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 40 + rank, busy);
@@ -1944,7 +1961,7 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
       atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 480 + min((hi - lo) >> 3, 15), 1ull);
       atomicAdd(reinterpret_cast<unsigned long long*>(P.prof) + 496 + (int)min(busy >> 12, 15ull), 1ull);
     }
-    if (warp == 0) publish(par ^ 1, (unsigned long long)round + 2);
+    push_msg(par ^ 1, (unsigned long long)round + 2);
     rebuild_after();
   }
   if (rank == 0 && tid == 0) {
