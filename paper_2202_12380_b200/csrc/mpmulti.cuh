@@ -1489,51 +1489,51 @@ __global__ void __launch_bounds__(MPG_LB_THREADS, 1) mp_multi_kernel(const LoopP
         }
       }
       auto item_scan = [&](int Gsc) {
-          // this CTA's items (tile pairs of its rows) and tiles of (g, v), at index
-          // t = g * 16 + v (g-major; v >= W contribute nothing): lane handles IPL pairs
-          const int GW = Gsc * 16;
-          int r4[IPL], t4[IPL], rs = 0, ts = 0;
-          // a lane's IPL entries share one candidate g (16 % IPL == 0): its window position
-          const int pq = st->pick[((lane * IPL) >> 4) & (BMAX - 1)];
+        // this CTA's items (tile pairs of its rows) and tiles of (g, v), at index
+        // t = g * 16 + v (g-major; v >= W contribute nothing): lane handles IPL pairs
+        const int GW = Gsc * 16;
+        int r4[IPL], t4[IPL], rs = 0, ts = 0;
+        // a lane's IPL entries share one candidate g (16 % IPL == 0): its window position
+        const int pq = st->pick[((lane * IPL) >> 4) & (BMAX - 1)];
 #pragma unroll
-          for (int q = 0; q < IPL; ++q) {
-            const int t = lane * IPL + q;
-            int nrw = 0, ntl = 0;
-            const int v = t & 15;
-            if (t < GW && v < W && !floorm) {
-              const int2 cn2 = ecnt[pq * 16 + v];
-              nrw = cn2.x;
-              ntl = cn2.y;
-            }
-            r4[q] = nrw;
-            t4[q] = ntl;
-            rs += nrw;
-            ts += ntl;
+        for (int q = 0; q < IPL; ++q) {
+          const int t = lane * IPL + q;
+          int nrw = 0, ntl = 0;
+          const int v = t & 15;
+          if (t < GW && v < W && !floorm) {
+            const int2 cn2 = ecnt[pq * 16 + v];
+            nrw = cn2.x;
+            ntl = cn2.y;
           }
-          int ri = rs, ti = ts;
+          r4[q] = nrw;
+          t4[q] = ntl;
+          rs += nrw;
+          ts += ntl;
+        }
+        int ri = rs, ti = ts;
 #pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int y1 = __shfl_up_sync(0xffffffffu, ri, o), y2 = __shfl_up_sync(0xffffffffu, ti, o);
-            if (lane >= o) {
-              ri += y1;
-              ti += y2;
-            }
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y1 = __shfl_up_sync(0xffffffffu, ri, o), y2 = __shfl_up_sync(0xffffffffu, ti, o);
+          if (lane >= o) {
+            ri += y1;
+            ti += y2;
           }
-          int rr = ri - rs, tt = ti - ts;
+        }
+        int rr = ri - rs, tt = ti - ts;
 #pragma unroll
-          for (int q = 0; q < IPL; ++q) {
-            const int t = lane * IPL + q;
-            if (t <= GW) {
-              st->ibase[t] = rr;
-              st->tbase[t] = tt;
-            }
-            rr += r4[q];
-            tt += t4[q];
+        for (int q = 0; q < IPL; ++q) {
+          const int t = lane * IPL + q;
+          if (t <= GW) {
+            st->ibase[t] = rr;
+            st->tbase[t] = tt;
           }
-          if (lane == 31 && GW == BMAX * 16) {
-            st->ibase[GW] = ri;
-            st->tbase[GW] = ti;
-          }
+          rr += r4[q];
+          tt += t4[q];
+        }
+        if (lane == 31 && GW == BMAX * 16) {
+          st->ibase[GW] = ri;
+          st->tbase[GW] = ti;
+        }
       };
       if (MPG_SCAN_W1 && warp == 1) {   // (NW >= 2) waits for the walk's picks, then the item bases
         bar_sync(1, 64);
