@@ -359,6 +359,29 @@ def test_multi_selection_grid_mode_bitwise_identical(mpg, name, prec, K):
     mp.close()
 
 
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_multi_selection_grid_long_c4(mpg, prec):
+    # a longer C4 run (25k atoms: thousands of rounds, hundreds of roll-backs, candidate-list
+    # rebuilds in every CTA) on the 128-CTA grid against the one-selection 16-CTA cluster,
+    # bit for bit -- the two-stage window ranking of the grid kernels at length
+    cfg = CONFIGS["C4"]
+    x, S = setup_of("C4")
+    xd = torch.from_numpy(x).cuda()
+    K = 25000
+    mp = mpg.MPGabor(cfg.dicts, cfg.thr, prec)
+    mp.set_batch(1)
+    mp.set_launch(16, 0, 0, 0)
+    ref = mp.run(xd, K, cfg.errdb)
+    res_ref = mp.residual(cfg.Ls).cpu().numpy()
+    mp.set_batch(8)
+    mp.set_launch(128, 0, 0, 0)
+    out = mp.run(xd, K, cfg.errdb)
+    assert mp.launch_info()["cluster"] == 128 and out.rounds < 0.6 * out.n
+    assert out.atoms.tobytes() == ref.atoms.tobytes() and out.energy.tobytes() == ref.energy.tobytes()
+    assert np.array_equal(mp.residual(cfg.Ls).cpu().numpy(), res_ref)
+    mp.close()
+
+
 @pytest.mark.parametrize("name,C", [("C3", 64), ("C4", 128)])
 def test_automatic_grid_multi_selection(mpg, name, C):
     # wide updates: the automatic choice runs multi-selection rounds on a grid of CTAs
